@@ -1,0 +1,425 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native EET decoder path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c3|c4|c5] [--batch B]
+
+Default workload (BASELINE.json configs[1], the metric's GPT-2-medium case):
+GPT-2-medium shape (h=1024, 24 layers, 16 heads, vocab 50257, s_max 1024),
+fp16, 16 prompts of 512 tokens + 512 greedy tokens through the public
+``generate`` API. One "step" = one full generate call (prompt pass + 512
+decode steps). ``value`` = generated tokens/s over the K timed steps, device
+time (CUDA events, max over ranks); ``e2e`` = the same through the public API
+by wall clock including the pinned H2D prompt copy and D2H token read.
+
+Multi-GPU (torchrun, one process per GPU): each rank runs its own batch
+(batch-sharded data parallelism, no collective on the data path); value =
+all ranks' tokens / max-over-ranks time ("scaling": "weak").
+
+Per-kernel roofline numbers come from a profiled replay of one step (eager,
+every launch bracketed by CUDA events on its launching stream, tagged with
+its algorithmic bytes/flops by the C ABI profiler). The CPU baseline times
+the oracle port of the reference path (oracle/, numpy + OpenBLAS on all host
+cores) on a bounded sample and extrapolates (stated in the output).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = None
+try:
+    with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+        METRIC = json.load(fh)["metric"]
+except Exception:
+    METRIC = "decoder-layer tokens/s at h768-12288, s<=4096; GPT-2-med 512-tok gen latency"
+
+WORKLOADS = {
+    # name: (hidden, layers, heads, vocab, prompt lengths spec, steps, dtype, batch)
+    "c2": dict(hidden=1024, layers=24, heads=16, vocab=50257, prompt=512, steps=512,
+               max_seq=1024, dtype="fp16", batch=16,
+               desc="GPT-2 medium (h1024, 24L, 16 heads, V50257), prompt 512 + greedy 512, fp16"),
+    "c1": dict(hidden=768, layers=1, heads=12, batch=4, prompt=64, dtype="fp32", kind="layer",
+               lengths="ratio0.2", desc="decoder layer h768 12 heads b4 s64 (pad 0.2), fp32"),
+    "c3": dict(hidden=2048, layers=1, heads=16, batch=32, prompt=1024, dtype="bf16", kind="layer",
+               lengths="ragged3", desc="decoder layer h2048 16 heads s1024 b32 ragged, bf16"),
+    "c4": dict(hidden=4096, layers=1, heads=32, batch=8, prompt=4096, dtype="bf16", kind="layer",
+               lengths="full", desc="decoder layer h4096 32 heads s4096 b8 context phase, bf16"),
+    "c5": dict(hidden=12288, layers=1, heads=96, batch=1, prompt=2048, dtype="bf16", kind="layer",
+               lengths="full", desc="decoder layer h12288 96 heads s2048 b1, bf16"),
+}
+
+HBM_KINDS = {"attn_decode", "gemv", "layernorm", "embed", "argmax", "softmax", "advance"}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def lengths_for(w):
+    from oracle import eet_oracle as orc
+    b, s = w["batch"], w["prompt"]
+    spec = w.get("lengths", "full")
+    if spec == "full":
+        return [s] * b
+    if spec == "ratio0.2":
+        return orc.lengths_for_ratio(b, s, 0.2)
+    if spec == "ragged3":
+        return [s] + [int(v) for v in np.random.default_rng(3).integers(1, s + 1, b - 1)]
+    raise ValueError(spec)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [v for v in sm if v > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU side
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_generate_sample(w, reps: int = 1):
+    """Bounded sample of the reference path (oracle port, numpy + OpenBLAS on
+    all cores) for the generate workload, extrapolated to the full job:
+    total = L * T(prompt layer) + head + steps * (L * T(step layer at the mean
+    cache length) + head). Returns (tokens/s, sample description)."""
+    from oracle import eet_oracle as orc
+    b, h, heads, V, p, steps, L = (w["batch"], w["hidden"], w["heads"], w["vocab"], w["prompt"],
+                                   w["steps"], w["layers"])
+    model = orc.seeded_weights(h, 1, heads, V, w["max_seq"], 0)
+    rng = np.random.default_rng(0)
+    pads = (0,) * b
+    x = rng.normal(0, 1, size=(b, p, h)).astype(np.float32)
+    best = None
+    for _ in range(reps):
+        kv = orc.OracleKV(b, heads, w["max_seq"], h // heads, 1)
+        t0 = time.perf_counter()
+        orc.decoder_layer(x, model.layers[0], kv, pads, 0, heads)
+        t_prompt = time.perf_counter() - t0
+        Lmean = p + steps // 2
+        kv.filled = Lmean - 1
+        x1 = x[:, :1]
+        t0 = time.perf_counter()
+        for _ in range(3):
+            orc.decoder_layer(x1, model.layers[0], kv, pads, 0, heads)
+        t_step = (time.perf_counter() - t0) / 3
+        t0 = time.perf_counter()
+        for _ in range(3):
+            np.argmax(orc.head_logits(model, x[:, -1]), axis=1)
+        t_head = (time.perf_counter() - t0) / 3
+        total = L * t_prompt + t_head + steps * (L * t_step + t_head)
+        best = total if best is None else min(best, total)
+    sample = (f"1 prompt layer (b{b} s{p}) + 3 decode layer steps at cache length {p + steps // 2} "
+              f"+ 3 LM heads, extrapolated x{L} layers x{steps} steps")
+    return b * steps / best, sample
+
+
+def cpu_layer_sample(w):
+    """One PROMPT_PARALLEL decoder layer on the oracle port: valid tokens/s."""
+    from oracle import eet_oracle as orc
+    lens = lengths_for(w)
+    b, h, heads = w["batch"], w["hidden"], w["heads"]
+    if b * max(lens) * h > 64 * 1024 * 1024 or h >= 4096:
+        # bounded: time one sequence and scale linearly (sequences independent)
+        lens1 = [max(lens)]
+        scale_b = sum(lens) / max(lens)
+    else:
+        lens1, scale_b = lens, 1.0
+    pads = orc.left_pads(lens1)
+    s = max(lens1)
+    model = orc.seeded_weights(h, 1, heads, 8, s, 0)
+    x = np.random.default_rng(1).normal(0, 1, size=(len(lens1), s, h)).astype(np.float32)
+    kv = orc.OracleKV(len(lens1), heads, s, h // heads, 1)
+    t0 = time.perf_counter()
+    orc.decoder_layer(x, model.layers[0], kv, pads, 0, heads)
+    dt = time.perf_counter() - t0
+    sample = f"one layer over {len(lens1)} sequence(s) of {s}" + (
+        f", scaled linearly to {b} sequences" if scale_b != 1.0 else "")
+    return sum(lens1) / dt, sample          # time is linear in tokens: same rate
+
+
+# ------------------------------------------------------------------ main
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, w, ws, rank):
+    if rank != 0:
+        return
+    reps = []
+    sample = ""
+    kind = w.get("kind", "generate")
+    for i in range(args.warmup + args.steps):
+        v, sample = cpu_generate_sample(w) if kind == "generate" else cpu_layer_sample(w)
+        if i >= args.warmup:
+            reps.append(v)
+    value = statistics.median(reps)
+    cores = cpu_threads()
+    unit = "tokens/s"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded random weights and tokens)",
+        "config": {"workload": w["desc"], "batch": w["batch"]},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    args = ap.parse_args()
+    w = dict(WORKLOADS[args.workload])
+    if args.batch:
+        w["batch"] = args.batch
+    ws, rank, local = dist_env()
+    args.gpus = ws if ws > 1 else args.gpus
+    if args.impl == "reference":
+        return run_reference(args, w, ws, rank)
+
+    import torch
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2104_12470_b200 as eet
+    from paper_2104_12470_b200 import _lib
+
+    kind = w.get("kind", "generate")
+    hbm, tflops, peak_src = peaks()
+    if kind == "generate":
+        cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=w["layers"],
+                              head_count=w["heads"], max_prompt=w["prompt"], max_sequence=w["max_seq"],
+                              datatype_label=w["dtype"])
+        weights = eet.random_weights(cfg, w["vocab"], seed=0)
+        rng = np.random.default_rng(rank)
+        prompts = [[int(t) for t in rng.integers(0, w["vocab"], size=w["prompt"])] for _ in range(w["batch"])]
+        req = eet.GenerationRequest(prompts=prompts, steps=w["steps"])
+        pool = eet.BufferPool()
+        units = w["batch"] * w["steps"]            # generated tokens per step
+        h2d, d2h = w["batch"] * w["prompt"] * 4, w["batch"] * w["steps"] * 8
+
+        def step(graph=True):
+            return eet.generate(weights, req, cfg, pool=pool, use_graph=graph)
+    else:
+        lens = lengths_for(w)
+        desc = eet.make_batch(lens)
+        s = desc.seq_len
+        cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=1,
+                              head_count=w["heads"], max_prompt=s, max_sequence=s,
+                              datatype_label=w["dtype"])
+        lw = eet.random_weights(eet.ModelConfig(1, w["hidden"], 1, w["heads"], 1, 1), 8, seed=0).layers[0]
+        kv, acts = eet.preallocate_caches(cfg)
+        pool = eet.BufferPool()
+        x_host = np.random.default_rng(1).normal(0, 1, size=(w["batch"], s, w["hidden"])).astype(np.float32)
+        x_dev = torch.from_numpy(x_host).cuda()
+        x_pin = torch.from_numpy(x_host).pin_memory()
+        units = sum(lens)
+        h2d = d2h = x_host.nbytes
+
+        def step(graph=True, host=False):
+            kv._filled = 0
+            if host:                               # e2e: pinned host -> device -> host
+                xd = x_pin.to("cuda", non_blocking=True)
+                eet.decoder_layer_forward(xd, lw, kv, desc, eet.Phase.PROMPT_PARALLEL, pool, acts, 0)
+                return xd.to("cpu")
+            return eet.decoder_layer_forward(x_dev, lw, kv, desc, eet.Phase.PROMPT_PARALLEL, pool, acts, 0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = ws * units * args.steps / (ms / 1e3)
+
+    # end to end through the public API: host inputs in, host results out
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(host=True) if kind != "generate" else step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = ws * units * args.steps / e2e_s
+
+    extra = {}
+    if kind == "generate" and rank == 0:
+        # batch-1 latency of the same workload (BASELINE c2 also quotes b=1)
+        cfg1 = eet.ModelConfig(1, w["hidden"], w["layers"], w["heads"], w["prompt"], w["max_seq"],
+                               datatype_label=w["dtype"])
+        req1 = eet.GenerationRequest(prompts=prompts[:1], steps=w["steps"])
+        eet.generate(weights, req1, cfg1, pool=pool)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eet.generate(weights, req1, cfg1, pool=pool)
+        torch.cuda.synchronize()
+        extra["latency_b1_s"] = time.perf_counter() - t0
+
+    roofline, kernels = None, {}
+    if not args.no_profile and rank == 0:
+        _lib.profile_enable(True)
+        step(graph=False) if kind == "generate" else step()
+        torch.cuda.synchronize()
+        summ = _lib.profile_summary()
+        _lib.profile_enable(False)
+        total = sum(v[1] for v in summ.values()) or 1.0
+        for name, (n, kms, by, fl) in summ.items():
+            hbm_k = name in HBM_KINDS
+            ach = (by / (kms / 1e3) / 1e9) if hbm_k else (fl / (kms / 1e3) / 1e12)
+            kernels[name] = {"launches": n, "ms": round(kms, 4), "share": round(kms / total, 4),
+                             "achieved": round(ach, 2), "unit": "GB/s" if hbm_k else "TFLOP/s",
+                             "frac": round(ach / (hbm if hbm_k else tflops), 4)}
+        dom = max(summ, key=lambda k: summ[k][1])
+        n, kms, by, fl = summ[dom]
+        hbm_k = dom in HBM_KINDS
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
+        if os.path.exists(tf):
+            traffic = json.load(open(tf)).get(args.workload, {}).get(dom)
+        ach = kernels[dom]["achieved"]
+        roofline = {"kernel": dom, "bound": "hbm" if hbm_k else "tensor", "achieved": ach,
+                    "peak": hbm if hbm_k else tflops, "unit": "GB/s" if hbm_k else "TFLOP/s",
+                    "frac": round(ach / (hbm if hbm_k else tflops), 4), "traffic": traffic,
+                    "algorithmic_per_launch": (by if hbm_k else fl) / n,
+                    "avg_launch_us": kms / n * 1e3, "peak_source": peak_src,
+                    "timing": "profiled eager replay of one step, CUDA events per launch"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        v, sample = cpu_generate_sample(w) if kind == "generate" else cpu_layer_sample(w)
+        cpu = {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port", "sample": sample}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": {"fp16": "f16", "bf16": "bf16", "fp32": "f32"}[w["dtype"]],
+            "data": "synthetic (seeded random weights N(0,0.02), random token ids / hidden states)",
+            "config": {"workload": w["desc"], "batch_per_gpu": w["batch"],
+                       "parallelism": f"dp{ws}" if ws > 1 else "single",
+                       "l2": "working set (weights+KV) > 126 MB L2 every step; no flush needed",
+                       "tokens_per_step": units},
+            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "kernels": kernels,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * eet_b200.h — C ABI of the B200-native EET decoder-layer path.
+ *
+ * Plain pointers, sizes and a CUDA stream handle (passed as void*); no torch
+ * types. Every entry point returns an eet_status (0 = OK); eet_last_error()
+ * gives the message of the last failure on the calling thread. All compute
+ * entry points are stream-ordered and asynchronous.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/maskfold/<file>:<line>). The Python host package
+ * (paper_2104_12470_b200) binds this ABI with ctypes and mirrors the
+ * reference's operator names, argument meaning and error behaviour.
+ *
+ * Conventions
+ *   - dtype: EET_F32 (reference "fp32 mode"), EET_BF16, EET_F16.
+ *   - Weights are stored K-major ("[out, in]", i.e. the reference's x @ W with
+ *     W transposed once on upload); the fused QKV weight is [3h, h] = [Wq;Wk;Wv]^T.
+ *   - Hidden state x is float32 [b, t, h] with batch stride x_sb and slot
+ *     stride x_ss (elements), so the reference's strided activation view
+ *     acts.hidden[:b, :t] (runtime.py:407) is accepted as-is.
+ *   - Left padding (core.py:98-123): pads[b] in [0, seq_len); sequence b's
+ *     real tokens occupy slots [pads[b], seq_len).
+ *   - KV cache per layer: K and V each [b_max, heads, s_max, hd] in the layer
+ *     dtype (memory.py:237-307).
+ */
+#ifndef EET_B200_H
+#define EET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EET_OK = 0,
+  EET_ERR_SHAPE = 1,     /* maps to ValueError          */
+  EET_ERR_OVERFLOW = 2,  /* maps to CacheOverflowError  */
+  EET_ERR_CUDA = 3,      /* maps to RuntimeError        */
+  EET_ERR_POOL = 4,      /* maps to PoolError           */
+  EET_ERR_ARG = 5,       /* maps to ValueError          */
+  EET_ERR_UNSUPPORTED = 6
+} eet_status;
+
+typedef enum { EET_F32 = 0, EET_BF16 = 1, EET_F16 = 2 } eet_dtype;
+
+typedef enum { EET_SCOPE_WITHIN = 0, EET_SCOPE_ACROSS = 1 } eet_scope;
+
+typedef enum { EET_PHASE_PROMPT = 0, EET_PHASE_INCREMENTAL = 1 } eet_phase;
+
+/* ---------------------------------------------------------------- library */
+const char* eet_last_error(void);
+int eet_abi_version(void);
+/* Number of kernel launches issued by this library since load (the bench's
+ * gpu_launches evidence). */
+uint64_t eet_launch_count(void);
+
+/* Per-launch profiler (bench.py's roofline numbers): while enabled, each
+ * launch outside graph capture is bracketed by CUDA events on its own
+ * stream and tagged with its algorithmic bytes / flops. enable(1) resets.
+ * summary(kind): launches, summed device ms, bytes and flops of that kind. */
+int eet_profile_enable(int on);
+int eet_profile_kinds(void);
+const char* eet_profile_kind_name(int kind);
+int eet_profile_summary(int kind, uint64_t* count, double* total_ms,
+                        double* bytes, double* flops);
+
+/* ------------------------------------------------------------- folding plan
+ * Replaces folding.py:30-54 (plan_folding). Pure host arithmetic; the row
+ * kernels take their launch shape from it. */
+int eet_plan_folding(int logical_size, int unit_cap, int* fold_count,
+                     int* sub_block_count, int* threads_per_block);
+
+/* ------------------------------------------------------------ buffer pool
+ * Device arena with the reference's two-scope reuse policy and ledger
+ * (memory.py:136-214 BufferPool, :44-87 AllocationLog). Sizes are BYTES.
+ * WITHIN reuses an idle buffer only on exact capacity match; ACROSS reuses
+ * the first idle buffer (creation order) with capacity >= size; otherwise
+ * cudaMalloc. Buffers are never freed before eet_pool_destroy. */
+typedef struct eet_pool eet_pool;
+int eet_pool_create(eet_pool** out);
+/* device_backed = 0: an accounting-only arena (host allocations, same
+ * policy and ledger) for planning and CPU-side policy checks. */
+int eet_pool_create_ex(eet_pool** out, int device_backed);
+int eet_pool_destroy(eet_pool* pool);
+int eet_pool_request(eet_pool* pool, size_t bytes, int scope, const char* tag,
+                     int* handle, void** dptr, size_t* capacity, int* reused);
+/* bytes: the size the claim requested (recorded in the ledger). */
+int eet_pool_release(eet_pool* pool, int handle, size_t bytes);
+/* stats[0..3] = total_capacity, peak_in_use, malloc_count, reuse_count */
+int eet_pool_stats(eet_pool* pool, uint64_t stats[4]);
+int eet_pool_ledger_size(eet_pool* pool, size_t* n);
+/* buffer i in creation order: capacity (bytes) and whether it is idle */
+int eet_pool_buffer_count(eet_pool* pool, size_t* n);
+int eet_pool_buffer_info(eet_pool* pool, size_t i, uint64_t* capacity, int* idle);
+/* event: 0 request, 1 release; decision: 0 malloc, 1 reuse, 2 idle */
+int eet_pool_ledger_get(eet_pool* pool, size_t i, int* event, uint64_t* bytes,
+                        int* decision, char* tag, size_t tag_cap);
+
+/* ------------------------------------------------ operator-level kernels */
+/* In-place mask-fused softmax over [batch*heads, seq, seq] fp32 planes.
+ * causal=1: fused_causal_softmax (attention.py:73-104);
+ * causal=0: fused_padding_softmax (attention.py:107-135).
+ * d_pads: device int32[batch]. fold_cap: unit cap of the folding plan
+ * (folding.py:30-54; 0 = default 1024). */
+int eet_masked_softmax(float* scores, const int* d_pads, int batch, int heads,
+                       int seq, int causal, int fold_cap, void* stream);
+
+/* In-place decode-step softmax over [batch, heads, len] fp32, window
+ * [pads[b], len) (attention.py:138-163). */
+int eet_step_softmax(float* scores, const int* d_pads, int batch, int heads,
+                     int len, int fold_cap, void* stream);
+
+/* Row layer norm (runtime.py:83-94), fp32 in/out: y = LN(x)*g + b. */
+int eet_layer_norm(const float* x, const float* gamma, const float* beta,
+                   float* y, int rows, int hidden, int fold_cap, void* stream);
+
+/* Mask-fused multi-head attention, fp32 q/k/v/out [b, s, h]
+ * (mha_forward, attention.py:172-217). Pad-query rows come out zero; keys
+ * below pads[b] are never read. */
+int eet_mha_forward(const float* q, const float* k, const float* v, float* out,
+                    const int* d_pads, int batch, int seq, int hidden,
+                    int heads, int causal, void* stream);
+
+/* Dense C[M,N] = A[M,K] * B[N,K]^T (+bias) in the given dtype (fp32 accum);
+ * C is float32 [M, ldc]. Used by tests and the LM head. */
+int eet_gemm(int dtype, const void* A, const void* B, const float* bias,
+             float* C, int M, int N, int K, int ldc, void* stream);
+
+/* ------------------------------------------------------------ layer path */
+typedef struct {
+  const float* ln1_g; const float* ln1_b;      /* [h]                   */
+  const void*  wqkv;                           /* [3h, h]  layer dtype  */
+  const void*  wo;                             /* [h, h]                */
+  const float* ln2_g; const float* ln2_b;      /* [h]                   */
+  const void*  w1;                             /* [4h, h]               */
+  const void*  w2;                             /* [h, 4h]               */
+  const float* b_qkv; const float* b_o;        /* optional biases (NULL) */
+  const float* b_1;   const float* b_2;
+} eet_layer_weights;
+
+typedef struct eet_runtime eet_runtime;
+
+/* One runtime per (device, dtype, capacities). Owns device scratch for row
+ * maps and split-K partials; activation scratch comes from `pool`. */
+int eet_runtime_create(eet_runtime** out, int dtype, int hidden, int heads,
+                       int max_batch, int max_sequence, eet_pool* pool);
+int eet_runtime_destroy(eet_runtime* rt);
+
+/* decoder_layer_forward (runtime.py:217-263), in place on x.
+ *   phase PROMPT: t == seq_len, attends causally within the prompt and writes
+ *                 K/V for slots [kv_filled, kv_filled+t);
+ *   phase INCREMENTAL: t == 1, appends slot kv_filled and attends over
+ *                 [pads[b], kv_filled]. The caller advances the cursor.
+ * kcache/vcache: this layer's [b_max, heads, s_max, hd] tensors.
+ * h_pads: HOST int32[b]. Pad rows of x are neither read nor written. */
+int eet_decoder_layer_forward(eet_runtime* rt, float* x, long long x_sb,
+                              long long x_ss, int batch, int t,
+                              const eet_layer_weights* w, void* kcache,
+                              void* vcache, int kv_filled, const int* h_pads,
+                              int seq_len, int phase, void* stream);
+
+/* encoder_layer_forward (runtime.py:266-301): bidirectional, no cache. */
+int eet_encoder_layer_forward(eet_runtime* rt, float* x, long long x_sb,
+                              long long x_ss, int batch, int t,
+                              const eet_layer_weights* w, const int* h_pads,
+                              void* stream);
+
+/* ------------------------------------------------------------- generation */
+typedef struct {
+  int layers, vocab, max_sequence;
+  const void* tok_emb;       /* [vocab, h]  layer dtype      */
+  const void* pos_emb;       /* [s_max, h]  layer dtype      */
+  const eet_layer_weights* layer;   /* [layers]              */
+  const float* lnf_g; const float* lnf_b;
+  const void* head;          /* [vocab, h] K-major (output_head^T) */
+  void* const* kcache;       /* [layers] device pointers     */
+  void* const* vcache;
+  float* hidden;             /* activation cache [b_max, max_prompt, h] fp32 */
+  int max_prompt;
+} eet_model;
+
+/* generate (runtime.py:372-437): one prompt pass, then `steps` incremental
+ * steps captured once into a CUDA graph and replayed. Greedy argmax with
+ * the lowest id on ties. h_prompts: HOST int32 [batch, max_len] padded with
+ * anything past each length; h_lengths: HOST int32[batch].
+ * h_tokens: HOST int64 [batch, steps] (written on return).
+ * d_logits: optional DEVICE fp32 [steps, batch, vocab] (may be NULL).
+ * use_graph: 0 runs the decode step eagerly (debug). */
+int eet_generate(eet_runtime* rt, const eet_model* model,
+                 const int* h_prompts, const int* h_lengths, int batch,
+                 int max_len, int steps, long long* h_tokens, float* d_logits,
+                 int use_graph, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EET_B200_H */

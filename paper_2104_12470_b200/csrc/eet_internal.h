@@ -1,0 +1,164 @@
+// Internal declarations shared by the CUDA translation units of libeet_b200.
+// Not part of the public ABI (include/eet_b200.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <string>
+#include <atomic>
+
+#include "../../include/eet_b200.h"
+
+namespace eet {
+
+// ----------------------------------------------------------- error plumbing
+void set_error(const std::string& msg);
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Per-launch profiler (eet_profile_*): when enabled and the stream is not
+// capturing, each launch is bracketed by CUDA events on its own stream and
+// tagged with its algorithmic bytes / flops. Also counts every launch.
+enum KernelKind : int {
+  K_LAYERNORM = 0, K_SOFTMAX, K_EMBED, K_ARGMAX, K_ADVANCE, K_GEMM_F32, K_GEMV,
+  K_GEMM_TC, K_ATTN_PREFILL, K_ATTN_DECODE, K_KIND_COUNT
+};
+struct ProfScope {
+  int slot = -1;
+  cudaStream_t st;
+  ProfScope(int kind, cudaStream_t st, double bytes, double flops);
+  ~ProfScope();
+};
+
+struct Fail {
+  int code;
+};
+
+#define EET_CHECK_CUDA(expr)                                                   \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::eet::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+      throw ::eet::Fail{EET_ERR_CUDA};                                         \
+    }                                                                          \
+  } while (0)
+
+#define EET_REQUIRE(cond, code, msg)                                           \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      ::eet::set_error(msg);                                                   \
+      throw ::eet::Fail{code};                                                 \
+    }                                                                          \
+  } while (0)
+
+#define EET_LAUNCH_CHECK() EET_CHECK_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------ folding plan
+// folding.py:30-54: minimal k with ceil(n / 2^k) <= cap.
+struct FoldPlan {
+  int fold_count, sub_blocks, threads;
+};
+FoldPlan plan_folding(int logical, int cap);
+
+// --------------------------------------------------------------- epilogue
+// What a GEMM-like kernel does with accumulator element (m, n).
+enum EpiMode : int {
+  EPI_STORE_F32 = 0,  // out_f32[m*ldo + n] = acc + bias
+  EPI_STORE_T = 1,    // out_T[m*ldo + n]   = acc + bias          (layer dtype)
+  EPI_GELU_T = 2,     // out_T[m*ldo + n]   = gelu(acc + bias)
+  EPI_RESID = 3,      // x[b*x_sb + t*x_ss + n] += acc + bias      (row map)
+  EPI_QKV = 4,        // n<hq: q_T[m*hq+n]; else K/V cache scatter (row map)
+};
+
+struct Epi {
+  int mode = EPI_STORE_F32;
+  const float* bias = nullptr;
+  void* out = nullptr;
+  int ldo = 0;
+  // residual (EPI_RESID) / cache scatter (EPI_QKV): packed row m -> (b, t)
+  float* x = nullptr;
+  long long x_sb = 0, x_ss = 0;
+  const int2* rinfo = nullptr;
+  // EPI_QKV
+  void* kc = nullptr;
+  void* vc = nullptr;
+  int heads = 0, hd = 0, hq = 0, smax = 0;
+  const int* kv_start = nullptr;  // device scalar (may be null) ...
+  int kv_base = 0;                // ... plus this: first cache slot of the step
+};
+
+// ---------------------------------------------------------------- launchers
+// Row ops (rowops.cu)
+void launch_layer_norm(const float* x, long long x_sb, long long x_ss,
+                       const int2* rinfo, int rows, const float* g,
+                       const float* b, void* y, int y_dtype, int ldy, int h,
+                       int fold_cap, cudaStream_t st);
+void launch_masked_softmax(float* s, const int* pads, int batch, int heads,
+                           int seq, int causal, int fold_cap, cudaStream_t st);
+void launch_step_softmax(float* s, const int* pads, int batch, int heads,
+                         int len, int fold_cap, cudaStream_t st);
+void launch_embed_prompt(int dtype, const void* tok, const void* pos,
+                         const int* prompts, int max_len, const int* pads,
+                         float* x, long long x_sb, int batch, int t, int h,
+                         cudaStream_t st);
+void launch_embed_step(int dtype, const void* tok, const void* pos,
+                       const int* cur_tok, const int* pads,
+                       const int* d_filled, float* x, long long x_sb,
+                       int batch, int h, cudaStream_t st);
+void launch_argmax(const float* logits, int batch, int vocab, int* cur_tok,
+                   long long* tokens_out, int steps, const int* d_step,
+                   float* logits_all, cudaStream_t st);
+void launch_advance(int* d_filled, int* d_step, cudaStream_t st);
+
+// GEMMs (gemm_simt.cu / gemm_tc.cu). C = A[M,K] * B[N,K]^T, fp32 accumulate.
+void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M,
+                   int N, int K, const Epi& e, cudaStream_t st);
+void gemv_small_m(int dtype, const void* A, int lda, const void* B, int ldb,
+                  int M, int N, int K, const Epi& e, cudaStream_t st);
+void gemm_tc_sm100(int dtype, const void* A, int lda, const void* B, int ldb,
+                   int M, int N, int K, const Epi& e, cudaStream_t st);
+// Dispatch by dtype and M (the one GEMM entry the runtime uses).
+void gemm(int dtype, const void* A, int lda, const void* B, int ldb, int M,
+          int N, int K, const Epi& e, cudaStream_t st);
+
+// Attention (attention.cu)
+struct PrefillArgs {
+  int dtype;
+  const void* q; int ldq; const int* q_rowbase;   // q row = q_rowbase[b] + slot
+  const void* k; const void* v;                   // (b,head,slot,d) strides
+  long long k_sb, k_sh, k_ss;
+  void* o; int ldo; const int* o_rowbase;
+  const int* pads;
+  const int* h_pads;   // host copy for byte/flop accounting (may be null)
+  int batch, seq, heads, hd;
+  float scale;
+  int causal;
+  int zero_pad_rows;   // padded layout: write zero rows for pad queries
+};
+void launch_attn_prefill(const PrefillArgs& a, cudaStream_t st);
+
+struct DecodeArgs {
+  int dtype;
+  const void* q; int ldq;              // row b
+  const void* kc; const void* vc;      // [b, heads, smax, hd]
+  int batch, heads, hd, smax;
+  const int* pads;
+  const int* kv_start;                 // keys [pad_b, (*kv_start) + kv_base + 1)
+  int kv_base;
+  const int* h_pads;                   // host copies for byte accounting only
+  int L_host;                          // (-1: unknown, e.g. inside a graph)
+  float scale;
+  float* part;                         // [b, heads, splits, hd + 2]
+  int* counters;                       // [b * heads], zero on entry, left zero
+  void* o; int ldo;                    // row b
+  int splits;
+};
+void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
+int decode_splits(int batch, int heads, int smax);
+
+// dtype helpers
+inline size_t dtype_size(int dt) { return dt == EET_F32 ? 4 : 2; }
+
+}  // namespace eet

@@ -1,0 +1,258 @@
+// CUDA-core GEMMs:
+//  * gemm_f32_simt — true-fp32 FFMA GEMM for the reference's "fp32 mode"
+//    (no TF32: identical greedy tokens need ~1e-6 logit accuracy, SURVEY
+//    Appendix B.4). Replaces the OpenBLAS sgemm calls at runtime.py:131,136,
+//    188,210,212,344.
+//  * gemv_small_m — M <= 16 rows (decode steps, LM head): HBM-bound on the
+//    weight read, so it streams W with 128-bit loads and keeps the few
+//    activation rows in shared memory. Works for every dtype.
+// Both compute C = A[M,K] * B[N,K]^T with the fused epilogue of common.cuh.
+#include "common.cuh"
+
+namespace eet {
+
+// ------------------------------------------------------------- fp32 GEMM
+namespace {
+constexpr int BM = 64, BN = 64, BK = 16;
+}
+
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, int lda,
+                                                       const float* __restrict__ B, int ldb,
+                                                       int M, int N, int K, Epi e) {
+  __shared__ __align__(16) float As[2][BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  // loader mapping: 64 rows x 16 k = 1024 elements; thread -> row lr, k lk..lk+3
+  const int lr = tid >> 2, lk = (tid & 3) * 4;
+  float acc[4][4] = {};
+  float ra[4], rb[4];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int k = k0 + lk + j;
+      int am = m0 + lr, bn = n0 + lr;
+      ra[j] = (am < M && k < K) ? A[(long long)am * lda + k] : 0.f;
+      rb[j] = (bn < N && k < K) ? B[(long long)bn * ldb + k] : 0.f;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      As[buf][lk + j][lr] = ra[j];
+      Bs[buf][lk + j][lr] = rb[j];
+    }
+  };
+  const int nk = (K + BK - 1) / BK;
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) gload((kt + 1) * BK);
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      float4 a = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+      float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+      float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) {
+      sstore(buf ^ 1);
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n < N) epi_apply<float>(e, m, n, acc[i][j]);
+    }
+  }
+}
+
+void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M, int N, int K,
+                   const Epi& e, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  ProfScope ps(K_GEMM_F32, st, gemm_bytes(M, N, K, 4, e), 2.0 * M * N * K);
+  gemm_f32_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e);
+  EET_LAUNCH_CHECK();
+}
+
+// --------------------------------------------------------- small-M GEMV
+// Block = 8 warps; warp w owns COLS consecutive output columns. Each lane
+// streams 16-byte slices of the COLS weight rows and multiplies them with
+// the MT activation rows staged (chunk by chunk along K) in shared memory.
+template <typename T, int MT, int COLS, bool VEC>
+__global__ void __launch_bounds__(256) gemv_kernel(const T* __restrict__ A, int lda,
+                                                   const T* __restrict__ B, int ldb, int M,
+                                                   int N, int K, int KC, Epi e) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xs = reinterpret_cast<T*>(smem_raw);          // [MT][KC]
+  constexpr int E = VEC ? 16 / sizeof(T) : 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nbase = (blockIdx.x * 8 + warp) * COLS;
+  float acc[COLS][MT];
+#pragma unroll
+  for (int c = 0; c < COLS; ++c)
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[c][m] = 0.f;
+
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    const int kc = min(KC, K - k0);
+    __syncthreads();
+    // stage activation rows [0, M) x [k0, k0+kc)
+    if constexpr (VEC) {
+      const int nv = kc / E;
+      for (int idx = threadIdx.x; idx < M * nv; idx += blockDim.x) {
+        int m = idx / nv, v = idx - m * nv;
+        *reinterpret_cast<uint4*>(xs + m * KC + v * E) =
+            *reinterpret_cast<const uint4*>(A + (long long)m * lda + k0 + v * E);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < M * kc; idx += blockDim.x) {
+        int m = idx / kc, k = idx - m * kc;
+        xs[m * KC + k] = A[(long long)m * lda + k0 + k];
+      }
+    }
+    __syncthreads();
+    for (int kk = lane * E; kk < kc; kk += 32 * E) {
+      float w[COLS][E];
+#pragma unroll
+      for (int c = 0; c < COLS; ++c) {
+        int n = nbase + c;
+        if (n < N) {
+          const T* src = B + (long long)n * ldb + k0 + kk;
+          if constexpr (VEC) {
+            load16<T>(src, w[c]);
+          } else {
+            w[c][0] = to_f(src[0]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < E; ++j) w[c][j] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        if (m < M) {
+          float xv[E];
+          if constexpr (VEC) {
+            load16<T>(xs + m * KC + kk, xv);
+          } else {
+            xv[0] = to_f(xs[m * KC + kk]);
+          }
+#pragma unroll
+          for (int c = 0; c < COLS; ++c)
+#pragma unroll
+            for (int j = 0; j < E; ++j) acc[c][m] = fmaf(w[c][j], xv[j], acc[c][m]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < COLS; ++c)
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[c][m] = warp_sum(acc[c][m]);
+#pragma unroll
+  for (int c = 0; c < COLS; ++c)
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      int p = c * MT + m;
+      if ((p & 31) == lane && m < M && nbase + c < N) epi_apply<T>(e, m, nbase + c, acc[c][m]);
+    }
+}
+
+template <typename T, int MT>
+static void gemv_launch(const T* A, int lda, const T* B, int ldb, int M, int N, int K,
+                        const Epi& e, cudaStream_t st) {
+  constexpr int COLS = 4;
+  constexpr int E = 16 / sizeof(T);
+  const bool vec = (K % E == 0) && (lda % E == 0) && (ldb % E == 0) &&
+                   ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+  int KC = (int)(65536 / (MT * sizeof(T)));          // 64 KB of staged activations
+  KC = std::min(KC, (K + E - 1) / E * E);
+  KC = std::max(E, KC / E * E);
+  size_t smem = (size_t)MT * KC * sizeof(T);
+  dim3 grid((N + 8 * COLS - 1) / (8 * COLS));
+  ProfScope ps(K_GEMV, st, gemm_bytes(M, N, K, sizeof(T), e), 2.0 * M * N * K);
+  if (vec) {
+    auto k = gemv_kernel<T, MT, COLS, true>;
+    EET_CHECK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 256, smem, st>>>(A, lda, B, ldb, M, N, K, KC, e);
+  } else {
+    auto k = gemv_kernel<T, MT, COLS, false>;
+    EET_CHECK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, 256, smem, st>>>(A, lda, B, ldb, M, N, K, KC, e);
+  }
+  EET_LAUNCH_CHECK();
+}
+
+template <typename T>
+static void gemv_dispatch(const T* A, int lda, const T* B, int ldb, int M, int N, int K,
+                          const Epi& e, cudaStream_t st) {
+  if (M <= 1) gemv_launch<T, 1>(A, lda, B, ldb, M, N, K, e, st);
+  else if (M <= 2) gemv_launch<T, 2>(A, lda, B, ldb, M, N, K, e, st);
+  else if (M <= 4) gemv_launch<T, 4>(A, lda, B, ldb, M, N, K, e, st);
+  else if (M <= 8) gemv_launch<T, 8>(A, lda, B, ldb, M, N, K, e, st);
+  else gemv_launch<T, 16>(A, lda, B, ldb, M, N, K, e, st);
+}
+
+void gemv_small_m(int dtype, const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+                  const Epi& e, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  EET_REQUIRE(M <= 16, EET_ERR_ARG, "gemv_small_m: M > 16");
+  switch (dtype) {
+    case EET_F32: gemv_dispatch<float>((const float*)A, lda, (const float*)B, ldb, M, N, K, e, st); break;
+    case EET_BF16: gemv_dispatch<__nv_bfloat16>((const __nv_bfloat16*)A, lda, (const __nv_bfloat16*)B, ldb, M, N, K, e, st); break;
+    default: gemv_dispatch<__half>((const __half*)A, lda, (const __half*)B, ldb, M, N, K, e, st);
+  }
+}
+
+// The GEMM entry the runtime uses: fp32 mode -> FFMA kernels; 16-bit modes ->
+// tcgen05 tensor cores (TMA-fed), with the HBM-bound small-M case on the
+// streaming GEMV.
+static bool tc_eligible(const void* A, int lda, const void* B, int ldb, int K) {
+  return (K % 8 == 0) && (lda % 8 == 0) && (ldb % 8 == 0) &&
+         ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+}
+
+void gemm(int dtype, const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+          const Epi& e, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return;
+  if (M <= 16) {
+    gemv_small_m(dtype, A, lda, B, ldb, M, N, K, e, st);
+    return;
+  }
+  if (dtype == EET_F32) {
+    gemm_f32_simt((const float*)A, lda, (const float*)B, ldb, M, N, K, e, st);
+    return;
+  }
+  if (tc_eligible(A, lda, B, ldb, K)) {
+    gemm_tc_sm100(dtype, A, lda, B, ldb, M, N, K, e, st);
+    return;
+  }
+  // 16-bit operands whose rows are not 16-byte aligned (tiny hidden sizes in
+  // tests): stream them through the GEMV 16 rows at a time.
+  const size_t es = dtype_size(dtype);
+  for (int m0 = 0; m0 < M; m0 += 16) {
+    Epi em = e;
+    // shift row-indexed epilogue state to the chunk
+    if (e.mode == EPI_RESID || e.mode == EPI_QKV) em.rinfo = e.rinfo + m0;
+    if (e.mode == EPI_QKV) em.out = (char*)e.out + (size_t)m0 * e.hq * es;
+    else if (e.mode == EPI_STORE_F32) em.out = (char*)e.out + (size_t)m0 * e.ldo * 4;
+    else if (e.mode != EPI_RESID) em.out = (char*)e.out + (size_t)m0 * e.ldo * es;
+    gemv_small_m(dtype, (const char*)A + (size_t)m0 * lda * es, lda, B, ldb, std::min(16, M - m0),
+                 N, K, em, st);
+  }
+}
+
+}  // namespace eet

@@ -1,0 +1,352 @@
+// Thread-block-folded row kernels: LayerNorm (+ pad-skipping pack), the
+// operator-level mask-fused softmaxes, embeddings, argmax.
+//
+// Folding (folding.py:30-54, §2.2): a row of `n` work items is cut
+// into t = 2^k sub-blocks of `threads` lanes; lane `tid` of the CTA owns items
+// sb*threads + tid for sb < t (folding.py:57-70 map_index). One launch shape
+// therefore covers h up to 16384 and seq up to 4096 with <= 1024 threads.
+#include "common.cuh"
+
+namespace eet {
+
+FoldPlan plan_folding(int logical, int cap) {
+  if (cap < 1) cap = 1024;
+  int k = 0;
+  while (((logical + (1 << k) - 1) >> k) > cap) ++k;
+  int t = 1 << k;
+  return FoldPlan{k, t, (logical + t - 1) / t};
+}
+
+static inline int round32(int n) { return (n + 31) & ~31; }
+
+// ------------------------------------------------------------------ LayerNorm
+// y[r] = (x[r] - mean) / sqrt(var_pop + 1e-5) * g + b   (runtime.py:83-94)
+// Row r reads x at (rinfo[r].x, rinfo[r].y) when rinfo != null (pad-skipping
+// pack: only valid tokens are normalised), else at r * x_sb. VEC float4 lanes
+// when h % 4 == 0. Two-pass (mean, then centred second moment) like numpy.
+template <typename TO, int VEC, int MAXT>
+__global__ void __launch_bounds__(1024) ln_kernel(
+    const float* __restrict__ x, long long x_sb, long long x_ss,
+    const int2* __restrict__ rinfo, const float* __restrict__ g,
+    const float* __restrict__ b, TO* __restrict__ y, int ldy, int h,
+    int sub_blocks, int lanes) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const float* xr;
+  if (rinfo) {
+    int2 ri = rinfo[r];
+    xr = x + ri.x * x_sb + ri.y * x_ss;
+  } else {
+    xr = x + (long long)r * x_sb;     // no row map: row r at batch stride
+  }
+  const int nvec = h / VEC;
+  float v[MAXT][VEC];
+  float s = 0.f;
+#pragma unroll
+  for (int sb = 0; sb < MAXT; ++sb) {
+    int i = sb * lanes + threadIdx.x;
+    bool ok = sb < sub_blocks && threadIdx.x < lanes && i < nvec;
+    if constexpr (VEC == 4) {
+      float4 q = ok ? reinterpret_cast<const float4*>(xr)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[sb][0] = q.x; v[sb][1] = q.y; v[sb][2] = q.z; v[sb][3] = q.w;
+    } else {
+      v[sb][0] = ok ? xr[i] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) s += v[sb][j];
+  }
+  const float mean = block_reduce<false>(s, red) / (float)h;
+  float q2 = 0.f;
+#pragma unroll
+  for (int sb = 0; sb < MAXT; ++sb) {
+    int i = sb * lanes + threadIdx.x;
+    bool ok = sb < sub_blocks && threadIdx.x < lanes && i < nvec;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      float d = v[sb][j] - mean;
+      q2 += ok ? d * d : 0.f;
+    }
+  }
+  const float var = block_reduce<false>(q2, red) / (float)h;
+  const float rstd = 1.0f / sqrtf(var + 1e-5f);
+  TO* yr = y + (long long)r * ldy;
+#pragma unroll
+  for (int sb = 0; sb < MAXT; ++sb) {
+    int i = sb * lanes + threadIdx.x;
+    if (!(sb < sub_blocks && threadIdx.x < lanes && i < nvec)) continue;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      int c = i * VEC + j;
+      yr[c] = from_f<TO>((v[sb][j] - mean) * rstd * g[c] + b[c]);
+    }
+  }
+}
+
+template <typename TO, int VEC>
+static void ln_dispatch(const float* x, long long x_sb, long long x_ss, const int2* rinfo, int rows,
+                        const float* g, const float* b, TO* y, int ldy, int h, int cap,
+                        cudaStream_t st) {
+  FoldPlan p = plan_folding(h / VEC, cap);
+  int threads = round32(p.threads);
+  EET_REQUIRE(threads <= 1024, EET_ERR_ARG, "layer norm: fold cap too large");
+#define LN_CASE(T_)                                                                      \
+  if (p.sub_blocks <= T_) {                                                              \
+    ProfScope ps(K_LAYERNORM, st, (double)rows * h * (4 + sizeof(TO)) + 8.0 * h, 8.0 * rows * h); \
+    ln_kernel<TO, VEC, T_><<<rows, threads, 0, st>>>(x, x_sb, x_ss, rinfo, g, b, y, ldy, h, \
+                                                    p.sub_blocks, p.threads);            \
+    EET_LAUNCH_CHECK();                                                                  \
+    return;                                                                              \
+  }
+  LN_CASE(1) LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(16)
+#undef LN_CASE
+  EET_REQUIRE(false, EET_ERR_UNSUPPORTED, "layer norm: hidden too large for the fold cap");
+}
+
+void launch_layer_norm(const float* x, long long x_sb, long long x_ss, const int2* rinfo,
+                       int rows, const float* g, const float* b, void* y, int y_dtype, int ldy,
+                       int h, int cap, cudaStream_t st) {
+  if (rows <= 0) return;
+  EET_REQUIRE(h >= 1 && h <= 16384, EET_ERR_ARG, "layer norm: hidden outside [1, 16384]");
+  bool v4 = (h % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
+            (x_ss % 4 == 0) && (x_sb % 4 == 0) && (rinfo || x_sb != 0);
+  switch (y_dtype) {
+    case EET_F32:
+      v4 ? ln_dispatch<float, 4>(x, x_sb, x_ss, rinfo, rows, g, b, (float*)y, ldy, h, cap, st)
+         : ln_dispatch<float, 1>(x, x_sb, x_ss, rinfo, rows, g, b, (float*)y, ldy, h, cap, st);
+      break;
+    case EET_BF16:
+      v4 ? ln_dispatch<__nv_bfloat16, 4>(x, x_sb, x_ss, rinfo, rows, g, b, (__nv_bfloat16*)y, ldy, h, cap, st)
+         : ln_dispatch<__nv_bfloat16, 1>(x, x_sb, x_ss, rinfo, rows, g, b, (__nv_bfloat16*)y, ldy, h, cap, st);
+      break;
+    default:
+      v4 ? ln_dispatch<__half, 4>(x, x_sb, x_ss, rinfo, rows, g, b, (__half*)y, ldy, h, cap, st)
+         : ln_dispatch<__half, 1>(x, x_sb, x_ss, rinfo, rows, g, b, (__half*)y, ldy, h, cap, st);
+  }
+}
+
+// ------------------------------------------------------- mask-fused softmax
+// One CTA per query row of one (batch, head) plane; window bounds come from
+// the row index and the sequence's pad offset — no mask tensor exists.
+// Window: causal [pad, i], bidirectional [pad, s); pad-query rows (i < pad)
+// and everything outside the window are written as exact zeros
+// (attention.py:73-135). Reductions run sub-block by sub-block in fixed
+// order, so results are deterministic for a fixed plan (attention.py:55-66).
+__global__ void __launch_bounds__(1024) masked_softmax_kernel(
+    float* __restrict__ s, const int* __restrict__ pads, int heads, int seq, int causal,
+    int sub_blocks, int lanes) {
+  __shared__ float red[32];
+  const int i = blockIdx.x;             // query row
+  const int plane = blockIdx.y;         // b * heads + head
+  const int pad = pads[plane / heads];
+  float* row = s + ((long long)plane * seq + i) * seq;
+  const int lo = pad, hi = causal ? i + 1 : seq;
+  const bool live = i >= pad;
+  float m = -INFINITY;
+  if (live) {
+    for (int sb = 0; sb < sub_blocks; ++sb) {
+      int j = sb * lanes + threadIdx.x;
+      if (threadIdx.x < lanes && j >= lo && j < hi) m = fmaxf(m, row[j]);
+    }
+  }
+  m = block_reduce<true>(m, red);
+  float sum = 0.f;
+  if (live) {
+    for (int sb = 0; sb < sub_blocks; ++sb) {
+      int j = sb * lanes + threadIdx.x;
+      if (threadIdx.x < lanes && j >= lo && j < hi) sum += expf(row[j] - m);
+    }
+  }
+  sum = block_reduce<false>(sum, red);
+  for (int sb = 0; sb < sub_blocks; ++sb) {
+    int j = sb * lanes + threadIdx.x;
+    if (threadIdx.x < lanes && j < seq) {
+      float o = 0.f;
+      if (live && j >= lo && j < hi) o = expf(row[j] - m) / sum;
+      row[j] = o;
+    }
+  }
+}
+
+void launch_masked_softmax(float* s, const int* pads, int batch, int heads, int seq, int causal,
+                           int cap, cudaStream_t st) {
+  if (batch * heads == 0 || seq == 0) return;
+  FoldPlan p = plan_folding(seq, cap);
+  int threads = round32(p.threads);
+  EET_REQUIRE(threads <= 1024, EET_ERR_ARG, "softmax: fold cap too large");
+  dim3 grid(seq, batch * heads);
+  ProfScope ps(K_SOFTMAX, st, 8.0 * batch * heads * seq * seq, 3.0 * batch * heads * seq * seq);
+  masked_softmax_kernel<<<grid, threads, 0, st>>>(s, pads, heads, seq, causal, p.sub_blocks,
+                                                  p.threads);
+  EET_LAUNCH_CHECK();
+}
+
+// Decode-step softmax over [b, heads, L]: window [pad_b, L) (attention.py:138-163).
+__global__ void __launch_bounds__(1024) step_softmax_kernel(
+    float* __restrict__ s, const int* __restrict__ pads, int heads, int len, int sub_blocks,
+    int lanes) {
+  __shared__ float red[32];
+  const int plane = blockIdx.x;
+  const int pad = pads[plane / heads];
+  float* row = s + (long long)plane * len;
+  float m = -INFINITY;
+  for (int sb = 0; sb < sub_blocks; ++sb) {
+    int j = sb * lanes + threadIdx.x;
+    if (threadIdx.x < lanes && j >= pad && j < len) m = fmaxf(m, row[j]);
+  }
+  m = block_reduce<true>(m, red);
+  float sum = 0.f;
+  for (int sb = 0; sb < sub_blocks; ++sb) {
+    int j = sb * lanes + threadIdx.x;
+    if (threadIdx.x < lanes && j >= pad && j < len) sum += expf(row[j] - m);
+  }
+  sum = block_reduce<false>(sum, red);
+
+  for (int sb = 0; sb < sub_blocks; ++sb) {
+    int j = sb * lanes + threadIdx.x;
+    if (threadIdx.x < lanes && j < len) row[j] = (j >= pad) ? expf(row[j] - m) / sum : 0.f;
+  }
+}
+
+void launch_step_softmax(float* s, const int* pads, int batch, int heads, int len, int cap,
+                         cudaStream_t st) {
+  if (batch * heads == 0 || len == 0) return;
+  FoldPlan p = plan_folding(len, cap);
+  int threads = round32(p.threads);
+  EET_REQUIRE(threads <= 1024, EET_ERR_ARG, "softmax: fold cap too large");
+  ProfScope ps(K_SOFTMAX, st, 8.0 * batch * heads * len, 3.0 * batch * heads * len);
+  step_softmax_kernel<<<batch * heads, threads, 0, st>>>(s, pads, heads, len, p.sub_blocks,
+                                                         p.threads);
+  EET_LAUNCH_CHECK();
+}
+
+// --------------------------------------------------------------- embeddings
+// Prompt: slot < pad -> zero row; else tok_emb[id] + pos_emb[slot - pad]
+// (runtime.py:304-323; logical positions).
+template <typename T>
+__global__ void embed_prompt_kernel(const T* __restrict__ tok, const T* __restrict__ pos,
+                                    const int* __restrict__ prompts, int max_len,
+                                    const int* __restrict__ pads, float* __restrict__ x,
+                                    long long x_sb, int t, int h) {
+  const int slot = blockIdx.x, b = blockIdx.y;
+  const int pad = pads[b];
+  float* xr = x + b * x_sb + (long long)slot * h;
+  if (slot < pad) {
+    for (int c = threadIdx.x; c < h; c += blockDim.x) xr[c] = 0.f;
+    return;
+  }
+  const int p = slot - pad;
+  const int id = prompts[b * max_len + p];
+  const T* tr = tok + (long long)id * h;
+  const T* pr = pos + (long long)p * h;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) xr[c] = to_f(tr[c]) + to_f(pr[c]);
+}
+
+// Step: one token per sequence at absolute slot *d_filled (runtime.py:326-338).
+template <typename T>
+__global__ void embed_step_kernel(const T* __restrict__ tok, const T* __restrict__ pos,
+                                  const int* __restrict__ cur, const int* __restrict__ pads,
+                                  const int* __restrict__ d_filled, float* __restrict__ x,
+                                  long long x_sb, int h) {
+  const int b = blockIdx.x;
+  const int p = *d_filled - pads[b];
+  const T* tr = tok + (long long)cur[b] * h;
+  const T* pr = pos + (long long)p * h;
+  float* xr = x + b * x_sb;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) xr[c] = to_f(tr[c]) + to_f(pr[c]);
+}
+
+void launch_embed_prompt(int dtype, const void* tok, const void* pos, const int* prompts,
+                         int max_len, const int* pads, float* x, long long x_sb, int batch, int t,
+                         int h, cudaStream_t st) {
+  dim3 grid(t, batch);
+  int threads = std::min(256, round32(h));
+  ProfScope ps(K_EMBED, st, (double)batch * t * h * (4 + 2 * dtype_size(dtype)), 1.0 * batch * t * h);
+  if (dtype == EET_F32)
+    embed_prompt_kernel<float><<<grid, threads, 0, st>>>((const float*)tok, (const float*)pos, prompts, max_len, pads, x, x_sb, t, h);
+  else if (dtype == EET_BF16)
+    embed_prompt_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>((const __nv_bfloat16*)tok, (const __nv_bfloat16*)pos, prompts, max_len, pads, x, x_sb, t, h);
+  else
+    embed_prompt_kernel<__half><<<grid, threads, 0, st>>>((const __half*)tok, (const __half*)pos, prompts, max_len, pads, x, x_sb, t, h);
+  EET_LAUNCH_CHECK();
+}
+
+void launch_embed_step(int dtype, const void* tok, const void* pos, const int* cur,
+                       const int* pads, const int* d_filled, float* x, long long x_sb, int batch,
+                       int h, cudaStream_t st) {
+  int threads = std::min(256, round32(h));
+  ProfScope ps(K_EMBED, st, (double)batch * h * (4 + 2 * dtype_size(dtype)), 1.0 * batch * h);
+  if (dtype == EET_F32)
+    embed_step_kernel<float><<<batch, threads, 0, st>>>((const float*)tok, (const float*)pos, cur, pads, d_filled, x, x_sb, h);
+  else if (dtype == EET_BF16)
+    embed_step_kernel<__nv_bfloat16><<<batch, threads, 0, st>>>((const __nv_bfloat16*)tok, (const __nv_bfloat16*)pos, cur, pads, d_filled, x, x_sb, h);
+  else
+    embed_step_kernel<__half><<<batch, threads, 0, st>>>((const __half*)tok, (const __half*)pos, cur, pads, d_filled, x, x_sb, h);
+  EET_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ argmax
+// Greedy next token, lowest id on ties (runtime.py:425, np.argmax). Also
+// records the token at step *d_step and optionally copies the logits row.
+__global__ void __launch_bounds__(1024) argmax_kernel(
+    const float* __restrict__ logits, int vocab, int* __restrict__ cur,
+    long long* __restrict__ toks, int steps, const int* __restrict__ d_step,
+    float* __restrict__ logits_all, int batch) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const int b = blockIdx.x;
+  const float* row = logits + (long long)b * vocab;
+  const int step = d_step ? *d_step : 0;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int j = threadIdx.x; j < vocab; j += blockDim.x) {
+    float v = row[j];
+    if (v > best || (v == best && j < bi)) { best = v; bi = j; }
+    if (logits_all && step < steps) logits_all[((long long)step * batch + b) * vocab + j] = v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { sv[wid] = best; si[wid] = bi; }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    best = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) {
+      if (bi == 0x7fffffff) bi = 0;      // all-NaN row: numpy returns 0
+      cur[b] = bi;
+      if (toks && step < steps) toks[(long long)b * steps + step] = bi;
+    }
+  }
+}
+
+void launch_argmax(const float* logits, int batch, int vocab, int* cur, long long* toks,
+                   int steps, const int* d_step, float* logits_all, cudaStream_t st) {
+  ProfScope ps(K_ARGMAX, st, 4.0 * batch * vocab * (logits_all ? 2 : 1), 1.0 * batch * vocab);
+  argmax_kernel<<<batch, 1024, 0, st>>>(logits, vocab, cur, toks, steps, d_step, logits_all,
+                                        batch);
+  EET_LAUNCH_CHECK();
+}
+
+__global__ void advance_kernel(int* d_filled, int* d_step) {
+  *d_filled += 1;
+  *d_step += 1;
+}
+
+void launch_advance(int* d_filled, int* d_step, cudaStream_t st) {
+  ProfScope ps(K_ADVANCE, st, 16.0, 2.0);
+  advance_kernel<<<1, 1, 0, st>>>(d_filled, d_step);
+  EET_LAUNCH_CHECK();
+}
+
+}  // namespace eet

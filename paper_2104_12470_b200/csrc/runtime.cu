@@ -1,0 +1,771 @@
+// C-ABI implementation (include/eet_b200.h): device buffer pool, operator
+// entry points, the decoder/encoder layer orchestration and the two-phase
+// generate loop with a CUDA-graph-captured decode step.
+#include "common.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace eet {
+
+static thread_local std::string t_err;
+std::atomic<uint64_t> g_launches{0};
+void set_error(const std::string& msg) { t_err = msg; }
+
+// ------------------------------------------------------------ profiler
+namespace {
+struct ProfRec {
+  int kind;
+  cudaEvent_t ev0, ev1;
+  double bytes, flops;
+};
+struct Profiler {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
+  size_t used = 0;
+} g_prof;
+
+const char* kKindNames[K_KIND_COUNT] = {"layernorm", "softmax", "embed", "argmax", "advance",
+                                        "gemm_f32", "gemv", "gemm_tc", "attn_prefill",
+                                        "attn_decode"};
+}  // namespace
+
+ProfScope::ProfScope(int kind, cudaStream_t s, double bytes, double flops) : st(s) {
+  count_launch();
+  if (!g_prof.on) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+  if (g_prof.used == g_prof.spare.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    g_prof.spare.push_back({a, b});
+  }
+  auto ev = g_prof.spare[g_prof.used++];
+  cudaEventRecord(ev.first, st);
+  slot = (int)g_prof.recs.size();
+  g_prof.recs.push_back(ProfRec{kind, ev.first, ev.second, bytes, flops});
+}
+
+ProfScope::~ProfScope() {
+  if (slot >= 0) cudaEventRecord(g_prof.recs[slot].ev1, st);
+}
+
+}  // namespace eet
+
+using namespace eet;
+
+#define EET_API_BEGIN try {
+#define EET_API_END                                                         \
+  }                                                                          \
+  catch (const Fail& f) {                                                    \
+    return f.code;                                                           \
+  }                                                                          \
+  catch (const std::exception& ex) {                                         \
+    set_error(ex.what());                                                    \
+    return EET_ERR_CUDA;                                                     \
+  }                                                                          \
+  return EET_OK;
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* eet_last_error(void) { return t_err.c_str(); }
+int eet_abi_version(void) { return 1; }
+uint64_t eet_launch_count(void) { return g_launches.load(); }
+
+int eet_profile_enable(int on) {
+  EET_API_BEGIN
+  EET_CHECK_CUDA(cudaDeviceSynchronize());
+  g_prof.on = on != 0;
+  g_prof.recs.clear();
+  g_prof.used = 0;
+  EET_API_END
+}
+
+int eet_profile_kinds(void) { return K_KIND_COUNT; }
+
+const char* eet_profile_kind_name(int kind) {
+  return (kind >= 0 && kind < K_KIND_COUNT) ? kKindNames[kind] : "";
+}
+
+int eet_profile_summary(int kind, uint64_t* count, double* total_ms, double* bytes,
+                        double* flops) {
+  EET_API_BEGIN
+  EET_CHECK_CUDA(cudaDeviceSynchronize());
+  uint64_t n = 0;
+  double ms = 0, by = 0, fl = 0;
+  for (const auto& r : g_prof.recs) {
+    if (r.kind != kind) continue;
+    float e = 0.f;
+    EET_CHECK_CUDA(cudaEventElapsedTime(&e, r.ev0, r.ev1));
+    ++n;
+    ms += e;
+    by += r.bytes;
+    fl += r.flops;
+  }
+  *count = n;
+  *total_ms = ms;
+  *bytes = by;
+  *flops = fl;
+  EET_API_END
+}
+
+int eet_plan_folding(int logical, int cap, int* k, int* t, int* n) {
+  EET_API_BEGIN
+  EET_REQUIRE(cap >= 1, EET_ERR_ARG, "unit_cap must be >= 1");
+  EET_REQUIRE(logical >= 1 && logical <= 16384, EET_ERR_ARG,
+              "logical_size outside supported range [1, 16384]");
+  FoldPlan p = plan_folding(logical, cap);
+  *k = p.fold_count;
+  *t = p.sub_blocks;
+  *n = p.threads;
+  EET_API_END
+}
+
+}  // extern "C"
+
+// ================================================================ pool
+// memory.py:136-214 policy on device memory; ledger mirrors AllocationLog.
+struct eet_pool {
+  struct Buf {
+    void* ptr;
+    size_t cap;
+    bool idle;
+    std::string tag;
+  };
+  struct Rec {
+    int event;      // 0 request, 1 release
+    uint64_t bytes;
+    int decision;   // 0 malloc, 1 reuse, 2 idle
+    std::string tag;
+  };
+  std::vector<Buf> bufs;
+  std::vector<Rec> ledger;
+  uint64_t in_use = 0, peak = 0, mallocs = 0, reuses = 0;
+  bool device = true;
+
+  ~eet_pool() {
+    for (auto& b : bufs) device ? (void)cudaFree(b.ptr) : std::free(b.ptr);
+  }
+
+  // returns handle index
+  int request(size_t bytes, int scope, const char* tag, void** ptr, bool* reused) {
+    EET_REQUIRE(bytes >= 1, EET_ERR_ARG, "buffer size must be >= 1");
+    EET_REQUIRE(scope == EET_SCOPE_WITHIN || scope == EET_SCOPE_ACROSS, EET_ERR_ARG,
+                "scope must be within or across");
+    int idx = -1;
+    for (size_t i = 0; i < bufs.size(); ++i) {
+      if (!bufs[i].idle) continue;
+      if (scope == EET_SCOPE_WITHIN ? bufs[i].cap == bytes : bufs[i].cap >= bytes) {
+        idx = (int)i;
+        break;
+      }
+    }
+    std::string t = tag ? tag : "";
+    if (idx < 0) {
+      void* p = nullptr;
+      if (device) {
+        EET_CHECK_CUDA(cudaMalloc(&p, bytes));
+      } else {
+        p = std::malloc(bytes);
+        EET_REQUIRE(p != nullptr, EET_ERR_CUDA, "host allocation failed");
+      }
+      bufs.push_back(Buf{p, bytes, false, t});
+      idx = (int)bufs.size() - 1;
+      ++mallocs;
+      ledger.push_back(Rec{0, bytes, 0, t});
+      *reused = false;
+    } else {
+      bufs[idx].idle = false;
+      bufs[idx].tag = t;
+      ++reuses;
+      ledger.push_back(Rec{0, bytes, 1, t});
+      *reused = true;
+    }
+    in_use += bufs[idx].cap;
+    peak = std::max(peak, in_use);
+    *ptr = bufs[idx].ptr;
+    return idx;
+  }
+
+  void release(int idx, size_t bytes) {
+    EET_REQUIRE(idx >= 0 && idx < (int)bufs.size(), EET_ERR_POOL, "unknown buffer handle");
+    EET_REQUIRE(!bufs[idx].idle, EET_ERR_POOL, "buffer handle released twice");
+    bufs[idx].idle = true;
+    in_use -= bufs[idx].cap;
+    ledger.push_back(Rec{1, bytes, 2, bufs[idx].tag});
+  }
+
+  uint64_t total() const {
+    uint64_t s = 0;
+    for (auto& b : bufs) s += b.cap;
+    return s;
+  }
+};
+
+// RAII claim used inside the layer orchestration.
+struct Claim {
+  eet_pool* pool;
+  int idx = -1;
+  size_t bytes = 0;
+  void* ptr = nullptr;
+  Claim(eet_pool* p, size_t b, int scope, const char* tag) : pool(p), bytes(b) {
+    bool r;
+    idx = pool->request(std::max<size_t>(b, 1), scope, tag, &ptr, &r);
+  }
+  void release() {
+    if (idx >= 0) pool->release(idx, bytes);
+    idx = -1;
+  }
+  ~Claim() {
+    if (idx >= 0) {
+      try { pool->release(idx, bytes); } catch (...) {}
+    }
+  }
+  template <typename P> P* as() const { return reinterpret_cast<P*>(ptr); }
+};
+
+extern "C" {
+
+int eet_pool_create(eet_pool** out) {
+  EET_API_BEGIN
+  *out = new eet_pool();
+  EET_API_END
+}
+
+int eet_pool_create_ex(eet_pool** out, int device_backed) {
+  EET_API_BEGIN
+  *out = new eet_pool();
+  (*out)->device = device_backed != 0;
+  EET_API_END
+}
+
+int eet_pool_destroy(eet_pool* pool) {
+  EET_API_BEGIN
+  delete pool;
+  EET_API_END
+}
+
+int eet_pool_request(eet_pool* pool, size_t bytes, int scope, const char* tag, int* handle,
+                     void** dptr, size_t* capacity, int* reused) {
+  EET_API_BEGIN
+  bool r = false;
+  int idx = pool->request(bytes, scope, tag, dptr, &r);
+  *handle = idx;
+  if (capacity) *capacity = pool->bufs[idx].cap;
+  if (reused) *reused = r ? 1 : 0;
+  EET_API_END
+}
+
+int eet_pool_release(eet_pool* pool, int handle, size_t bytes) {
+  EET_API_BEGIN
+  pool->release(handle, bytes);
+  EET_API_END
+}
+
+int eet_pool_stats(eet_pool* pool, uint64_t stats[4]) {
+  EET_API_BEGIN
+  stats[0] = pool->total();
+  stats[1] = pool->peak;
+  stats[2] = pool->mallocs;
+  stats[3] = pool->reuses;
+  EET_API_END
+}
+
+int eet_pool_ledger_size(eet_pool* pool, size_t* n) {
+  EET_API_BEGIN
+  *n = pool->ledger.size();
+  EET_API_END
+}
+
+int eet_pool_buffer_count(eet_pool* pool, size_t* n) {
+  EET_API_BEGIN
+  *n = pool->bufs.size();
+  EET_API_END
+}
+
+int eet_pool_buffer_info(eet_pool* pool, size_t i, uint64_t* capacity, int* idle) {
+  EET_API_BEGIN
+  EET_REQUIRE(i < pool->bufs.size(), EET_ERR_ARG, "buffer index out of range");
+  *capacity = pool->bufs[i].cap;
+  *idle = pool->bufs[i].idle ? 1 : 0;
+  EET_API_END
+}
+
+int eet_pool_ledger_get(eet_pool* pool, size_t i, int* event, uint64_t* bytes, int* decision,
+                        char* tag, size_t tag_cap) {
+  EET_API_BEGIN
+  EET_REQUIRE(i < pool->ledger.size(), EET_ERR_ARG, "ledger index out of range");
+  const auto& r = pool->ledger[i];
+  *event = r.event;
+  *bytes = r.bytes;
+  *decision = r.decision;
+  if (tag && tag_cap) {
+    std::strncpy(tag, r.tag.c_str(), tag_cap - 1);
+    tag[tag_cap - 1] = 0;
+  }
+  EET_API_END
+}
+
+// ============================================================ operators
+int eet_masked_softmax(float* scores, const int* d_pads, int batch, int heads, int seq, int causal,
+                       int fold_cap, void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(batch >= 1 && heads >= 1 && seq >= 1, EET_ERR_SHAPE, "softmax: empty shape");
+  launch_masked_softmax(scores, d_pads, batch, heads, seq, causal, fold_cap, S(stream));
+  EET_API_END
+}
+
+int eet_step_softmax(float* scores, const int* d_pads, int batch, int heads, int len, int fold_cap,
+                     void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(batch >= 1 && heads >= 1 && len >= 1, EET_ERR_SHAPE, "step softmax: empty shape");
+  launch_step_softmax(scores, d_pads, batch, heads, len, fold_cap, S(stream));
+  EET_API_END
+}
+
+int eet_layer_norm(const float* x, const float* g, const float* b, float* y, int rows, int h,
+                   int fold_cap, void* stream) {
+  EET_API_BEGIN
+  launch_layer_norm(x, h, h, nullptr, rows, g, b, y, EET_F32, h, h, fold_cap, S(stream));
+  EET_API_END
+}
+
+int eet_mha_forward(const float* q, const float* k, const float* v, float* out, const int* d_pads,
+                    int batch, int seq, int hidden, int heads, int causal, void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(heads >= 1 && hidden % heads == 0, EET_ERR_SHAPE, "hidden not divisible by heads");
+  PrefillArgs a{};
+  a.dtype = EET_F32;
+  a.q = q; a.ldq = hidden; a.q_rowbase = nullptr;
+  a.k = k; a.v = v;
+  a.k_sb = (long long)seq * hidden; a.k_sh = hidden / heads; a.k_ss = hidden;
+  a.o = out; a.ldo = hidden; a.o_rowbase = nullptr;
+  a.pads = d_pads;
+  a.batch = batch; a.seq = seq; a.heads = heads; a.hd = hidden / heads;
+  a.scale = 1.0f / std::sqrt((float)a.hd);
+  a.causal = causal;
+  a.zero_pad_rows = 1;
+  launch_attn_prefill(a, S(stream));
+  EET_API_END
+}
+
+int eet_gemm(int dtype, const void* A, const void* B, const float* bias, float* C, int M, int N,
+             int K, int ldc, void* stream) {
+  EET_API_BEGIN
+  Epi e;
+  e.mode = EPI_STORE_F32;
+  e.out = C;
+  e.ldo = ldc;
+  e.bias = bias;
+  gemm(dtype, A, K, B, K, M, N, K, e, S(stream));
+  EET_API_END
+}
+
+}  // extern "C"
+
+// ============================================================= runtime
+struct StepPlan {
+  int T = 0;               // packed (valid) rows
+  int batch = 0, t = 0;    // x is [batch, t, h]
+  int seq = 0;             // prompt length (prefill window)
+  int phase = EET_PHASE_PROMPT;
+  bool valid = false;
+  std::vector<int> h_pads; // host copy: uploads are skipped when unchanged
+  int2* rinfo = nullptr;   // [T] (b, t_local)
+  int* rowbase = nullptr;  // [b] packed row of slot s = rowbase[b] + s
+  int* pads = nullptr;     // [b]
+};
+
+struct eet_runtime {
+  int dtype, h, heads, hd, bmax, smax, splits;
+  eet_pool* pool;
+  cudaStream_t cs = nullptr;          // private stream for graph capture
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  StepPlan plans[3];                  // 0: layer API, 1: generate prompt, 2: generate step
+  std::vector<void*> owned;
+  float* part = nullptr;              // decode split partials
+  int* counters = nullptr;
+  int* d_prompts = nullptr;           // [bmax * smax]
+  int* d_filled = nullptr;
+  int* d_step = nullptr;
+  int* d_cur = nullptr;               // [bmax]
+  int* h_prompts = nullptr;           // pinned staging: prompts in, tokens out
+  long long* h_tokens = nullptr;
+
+  void* dev(size_t bytes) {
+    void* p = nullptr;
+    EET_CHECK_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    owned.push_back(p);
+    return p;
+  }
+  ~eet_runtime() {
+    for (void* p : owned) cudaFree(p);
+    if (h_prompts) cudaFreeHost(h_prompts);
+    if (h_tokens) cudaFreeHost(h_tokens);
+    if (cs) cudaStreamDestroy(cs);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+  }
+};
+
+static void plan_alloc(eet_runtime* rt, StepPlan& p) {
+  p.rinfo = (int2*)rt->dev(sizeof(int2) * (size_t)rt->bmax * rt->smax);
+  p.rowbase = (int*)rt->dev(sizeof(int) * rt->bmax);
+  p.pads = (int*)rt->dev(sizeof(int) * rt->bmax);
+}
+
+// Host-side packing of the valid tokens (pad skipping): prompt rows are the
+// slots [pad_b, t) of each sequence, incremental rows are every sequence.
+// The device copies are refreshed only when the batch layout changes.
+static void plan_fill(StepPlan& p, int batch, int t, const int* pads, int seq, int phase,
+                      cudaStream_t st) {
+  if (p.valid && p.batch == batch && p.t == t && p.seq == seq && p.phase == phase &&
+      std::equal(pads, pads + batch, p.h_pads.begin()))
+    return;
+  std::vector<int2> ri;
+  std::vector<int> rb(batch);
+  ri.reserve((size_t)batch * t);
+  for (int b = 0; b < batch; ++b) {
+    int first = (phase == EET_PHASE_PROMPT) ? pads[b] : 0;
+    rb[b] = (int)ri.size() - first;
+    for (int s = first; s < t; ++s) ri.push_back(make_int2(b, s));
+  }
+  p.T = (int)ri.size();
+  p.batch = batch;
+  p.t = t;
+  p.seq = seq;
+  p.phase = phase;
+  p.h_pads.assign(pads, pads + batch);
+  // pageable-source async copies return once the source is staged
+  if (!ri.empty())
+    EET_CHECK_CUDA(cudaMemcpyAsync(p.rinfo, ri.data(), sizeof(int2) * ri.size(),
+                                   cudaMemcpyHostToDevice, st));
+  EET_CHECK_CUDA(cudaMemcpyAsync(p.rowbase, rb.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, st));
+  EET_CHECK_CUDA(cudaMemcpyAsync(p.pads, pads, sizeof(int) * batch, cudaMemcpyHostToDevice, st));
+  p.valid = true;
+}
+
+// One pre-norm layer over a prepared plan (runtime.py:217-263):
+//   LN1 (gather valid rows) -> QKV GEMM (epilogue: Q packed, K/V -> cache)
+//   -> mask-fused attention -> out-proj GEMM (epilogue: x += .)
+//   -> LN2 -> W1 GEMM (epilogue: GELU) -> W2 GEMM (epilogue: x += .)
+// Cache slot of local position 0 = (kv_dev ? *kv_dev : 0) + kv_base; the
+// device form lets a captured decode step advance without re-capture.
+static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb,
+                       long long x_ss, const eet_layer_weights* w, void* kc, void* vc,
+                       const int* kv_dev, int kv_base, bool causal, int L_host, cudaStream_t st) {
+  const int h = rt->h, T = p.T, dt = rt->dtype;
+  const size_t es = dtype_size(dt);
+  const int scope = (p.phase == EET_PHASE_PROMPT) ? EET_SCOPE_WITHIN : EET_SCOPE_ACROSS;
+  if (T == 0) return;
+
+  Claim ln(rt->pool, (size_t)T * h * es, scope, "attention.layernorm");
+  launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln1_g, w->ln1_b, ln.ptr, dt, h, h, 0, st);
+
+  Claim q(rt->pool, (size_t)T * h * es, scope, "attention.query");
+  {
+    Epi e;
+    e.mode = EPI_QKV;
+    e.bias = w->b_qkv;
+    e.out = q.ptr;
+    e.rinfo = p.rinfo;
+    e.kc = kc;
+    e.vc = vc;
+    e.heads = rt->heads;
+    e.hd = rt->hd;
+    e.hq = h;
+    e.smax = rt->smax;
+    e.kv_start = kv_dev;
+    e.kv_base = kv_base;
+    gemm(dt, ln.ptr, h, w->wqkv, h, T, 3 * h, h, e, st);
+  }
+  ln.release();
+
+  Claim ctx(rt->pool, (size_t)T * h * es, scope, "attention.context");
+  const float scale = 1.0f / std::sqrt((float)rt->hd);
+  if (p.phase == EET_PHASE_PROMPT) {
+    PrefillArgs a{};
+    a.dtype = dt;
+    a.q = q.ptr; a.ldq = h; a.q_rowbase = p.rowbase;
+    a.k = kc; a.v = vc;
+    a.k_sb = (long long)rt->heads * rt->smax * rt->hd;
+    a.k_sh = (long long)rt->smax * rt->hd;
+    a.k_ss = rt->hd;
+    a.o = ctx.ptr; a.ldo = h; a.o_rowbase = p.rowbase;
+    a.pads = p.pads;
+    a.h_pads = p.h_pads.data();
+    a.batch = p.batch; a.seq = p.seq; a.heads = rt->heads; a.hd = rt->hd;
+    a.scale = scale;
+    a.causal = causal ? 1 : 0;
+    a.zero_pad_rows = 0;
+    launch_attn_prefill(a, st);
+  } else {
+    DecodeArgs a{};
+    a.dtype = dt;
+    a.q = q.ptr; a.ldq = h;
+    a.kc = kc; a.vc = vc;
+    a.batch = p.batch; a.heads = rt->heads; a.hd = rt->hd; a.smax = rt->smax;
+    a.pads = p.pads;
+    a.kv_start = kv_dev;
+    a.kv_base = kv_base;
+    a.h_pads = p.h_pads.data();
+    a.L_host = L_host;
+    a.scale = scale;
+    a.part = rt->part;
+    a.counters = rt->counters;
+    a.o = ctx.ptr; a.ldo = h;
+    a.splits = rt->splits;
+    launch_attn_decode(a, st);
+  }
+  q.release();
+  {
+    Epi e;
+    e.mode = EPI_RESID;
+    e.bias = w->b_o;
+    e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
+    e.rinfo = p.rinfo;
+    gemm(dt, ctx.ptr, h, w->wo, h, T, h, h, e, st);
+  }
+  ctx.release();
+
+  // feed-forward block: both requests use across-module scope (runtime.py:200-207)
+  Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
+  launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln2_g, w->ln2_b, ln2.ptr, dt, h, h, 0, st);
+  Claim mid(rt->pool, (size_t)T * 4 * h * es, EET_SCOPE_ACROSS, "ffn.intermediate");
+  {
+    Epi e;
+    e.mode = EPI_GELU_T;
+    e.bias = w->b_1;
+    e.out = mid.ptr;
+    e.ldo = 4 * h;
+    gemm(dt, ln2.ptr, h, w->w1, h, T, 4 * h, h, e, st);
+  }
+  {
+    Epi e;
+    e.mode = EPI_RESID;
+    e.bias = w->b_2;
+    e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
+    e.rinfo = p.rinfo;
+    gemm(dt, mid.ptr, 4 * h, w->w2, 4 * h, T, h, 4 * h, e, st);
+  }
+  mid.release();
+  ln2.release();
+}
+
+extern "C" {
+
+int eet_runtime_create(eet_runtime** out, int dtype, int hidden, int heads, int max_batch,
+                       int max_sequence, eet_pool* pool) {
+  EET_API_BEGIN
+  EET_REQUIRE(dtype == EET_F32 || dtype == EET_BF16 || dtype == EET_F16, EET_ERR_ARG, "bad dtype");
+  EET_REQUIRE(heads >= 1 && hidden % heads == 0, EET_ERR_ARG, "hidden not divisible by heads");
+  EET_REQUIRE(max_batch >= 1 && max_sequence >= 1, EET_ERR_ARG, "bad capacities");
+  EET_REQUIRE(pool != nullptr && pool->device, EET_ERR_ARG, "runtime needs a device-backed buffer pool");
+  std::unique_ptr<eet_runtime> rt(new eet_runtime());
+  rt->dtype = dtype;
+  rt->h = hidden;
+  rt->heads = heads;
+  rt->hd = hidden / heads;
+  rt->bmax = max_batch;
+  rt->smax = max_sequence;
+  rt->pool = pool;
+  rt->splits = decode_splits(max_batch, heads, max_sequence);
+  for (auto& p : rt->plans) plan_alloc(rt.get(), p);
+  rt->part = (float*)rt->dev(sizeof(float) * (size_t)max_batch * heads * rt->splits * (rt->hd + 2));
+  rt->counters = (int*)rt->dev(sizeof(int) * (size_t)max_batch * heads);
+  EET_CHECK_CUDA(cudaMemset(rt->counters, 0, sizeof(int) * (size_t)max_batch * heads));
+  rt->d_prompts = (int*)rt->dev(sizeof(int) * (size_t)max_batch * max_sequence);
+  rt->d_filled = (int*)rt->dev(sizeof(int));
+  rt->d_step = (int*)rt->dev(sizeof(int));
+  rt->d_cur = (int*)rt->dev(sizeof(int) * max_batch);
+  EET_CHECK_CUDA(cudaMallocHost(&rt->h_prompts, sizeof(int) * (size_t)max_batch * max_sequence));
+  EET_CHECK_CUDA(cudaMallocHost(&rt->h_tokens, sizeof(long long) * (size_t)max_batch * max_sequence));
+  EET_CHECK_CUDA(cudaStreamCreateWithFlags(&rt->cs, cudaStreamNonBlocking));
+  EET_CHECK_CUDA(cudaEventCreateWithFlags(&rt->ev_in, cudaEventDisableTiming));
+  EET_CHECK_CUDA(cudaEventCreateWithFlags(&rt->ev_out, cudaEventDisableTiming));
+  EET_CHECK_CUDA(cudaDeviceSynchronize());
+  *out = rt.release();
+  EET_API_END
+}
+
+int eet_runtime_destroy(eet_runtime* rt) {
+  EET_API_BEGIN
+  if (rt) cudaDeviceSynchronize();
+  delete rt;
+  EET_API_END
+}
+
+int eet_decoder_layer_forward(eet_runtime* rt, float* x, long long x_sb, long long x_ss, int batch,
+                              int t, const eet_layer_weights* w, void* kc, void* vc,
+                              int kv_filled, const int* h_pads, int seq_len, int phase,
+                              void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(batch >= 1 && batch <= rt->bmax, EET_ERR_SHAPE, "batch exceeds runtime capacity");
+  if (phase == EET_PHASE_INCREMENTAL) {
+    EET_REQUIRE(t == 1, EET_ERR_SHAPE, "incremental step takes 1 token");
+    EET_REQUIRE(kv_filled >= seq_len, EET_ERR_SHAPE, "incremental phase before the prompt was cached");
+  } else {
+    EET_REQUIRE(t == seq_len, EET_ERR_SHAPE, "prompt pass length does not match seq_len");
+    EET_REQUIRE(kv_filled == 0, EET_ERR_SHAPE, "prompt phase expects an empty cache");
+  }
+  EET_REQUIRE(kv_filled + t <= rt->smax, EET_ERR_OVERFLOW, "step would overflow the cache");
+  for (int b = 0; b < batch; ++b)
+    EET_REQUIRE(h_pads[b] >= 0 && h_pads[b] < seq_len, EET_ERR_SHAPE, "pad outside [0, seq_len)");
+  StepPlan& p = rt->plans[0];
+  plan_fill(p, batch, t, h_pads, seq_len, phase, S(stream));
+  layer_impl(rt, p, x, x_sb, x_ss, w, kc, vc, nullptr, kv_filled, true, kv_filled + t, S(stream));
+  EET_API_END
+}
+
+int eet_encoder_layer_forward(eet_runtime* rt, float* x, long long x_sb, long long x_ss, int batch,
+                              int t, const eet_layer_weights* w, const int* h_pads, void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(batch >= 1 && batch <= rt->bmax && t <= rt->smax, EET_ERR_SHAPE,
+              "encoder input exceeds runtime capacity");
+  for (int b = 0; b < batch; ++b)
+    EET_REQUIRE(h_pads[b] >= 0 && h_pads[b] < t, EET_ERR_SHAPE, "pad outside [0, seq_len)");
+  StepPlan& p = rt->plans[0];
+  plan_fill(p, batch, t, h_pads, t, EET_PHASE_PROMPT, S(stream));
+  // bidirectional attention reads K/V scattered into scratch [b, heads, smax, hd]
+  const size_t kvb = (size_t)batch * rt->heads * rt->smax * rt->hd * dtype_size(rt->dtype);
+  Claim kbuf(rt->pool, kvb, EET_SCOPE_WITHIN, "attention.key");
+  Claim vbuf(rt->pool, kvb, EET_SCOPE_WITHIN, "attention.value");
+  layer_impl(rt, p, x, x_sb, x_ss, w, kbuf.ptr, vbuf.ptr, nullptr, 0, false, t, S(stream));
+  EET_API_END
+}
+
+// ----------------------------------------------------------- generate
+static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long long x_sb,
+                      int slot, int batch, int steps, long long* d_tokens, float* d_logits,
+                      cudaStream_t st) {
+  const int h = rt->h, dt = rt->dtype;
+  const size_t es = dtype_size(dt);
+  // rows (b, slot) of x; a tiny row map lives in plan 2's rinfo tail
+  Claim ln(rt->pool, (size_t)batch * h * es, EET_SCOPE_ACROSS, "output.layernorm");
+  Claim lg(rt->pool, (size_t)batch * m->vocab * 4, EET_SCOPE_ACROSS, "output.logits");
+  launch_layer_norm(x + (long long)slot * h, x_sb, h, nullptr, batch, m->lnf_g, m->lnf_b, ln.ptr,
+                    dt, h, h, 0, st);
+  Epi e;
+  e.mode = EPI_STORE_F32;
+  e.out = lg.ptr;
+  e.ldo = m->vocab;
+  gemm(dt, ln.ptr, h, m->head, h, batch, m->vocab, h, e, st);
+  launch_argmax(lg.as<float>(), batch, m->vocab, rt->d_cur, d_tokens, steps, rt->d_step, d_logits,
+                st);
+  lg.release();
+  ln.release();
+}
+
+// L_host: keys attended this step when known on the host (-1 under capture)
+static void decode_iteration(eet_runtime* rt, const eet_model* m, int batch, int steps,
+                             long long* d_tokens, float* d_logits, int L_host, cudaStream_t st) {
+  const int h = rt->h;
+  const long long x_sb = (long long)m->max_prompt * h;
+  StepPlan& p = rt->plans[2];
+  launch_embed_step(rt->dtype, m->tok_emb, m->pos_emb, rt->d_cur, p.pads, rt->d_filled, m->hidden,
+                    x_sb, batch, h, st);
+  for (int l = 0; l < m->layers; ++l)
+    layer_impl(rt, p, m->hidden, x_sb, h, &m->layer[l], m->kcache[l], m->vcache[l], rt->d_filled,
+               0, true, L_host, st);
+  launch_advance(rt->d_filled, rt->d_step, st);
+  head_step(rt, m, m->hidden, x_sb, 0, batch, steps, d_tokens, d_logits, st);
+}
+
+int eet_generate(eet_runtime* rt, const eet_model* m, const int* h_prompts, const int* h_lengths,
+                 int batch, int max_len, int steps, long long* h_tokens, float* d_logits,
+                 int use_graph, void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(batch >= 1 && batch <= rt->bmax, EET_ERR_SHAPE, "batch exceeds configured maximum");
+  EET_REQUIRE(max_len >= 1 && max_len <= m->max_prompt, EET_ERR_SHAPE, "prompt exceeds max prompt");
+  EET_REQUIRE(max_len + steps <= rt->smax && max_len + steps <= m->max_sequence, EET_ERR_SHAPE,
+              "prompt + steps exceeds max sequence");
+  cudaStream_t caller = S(stream);
+  cudaStream_t st = rt->cs;
+  EET_CHECK_CUDA(cudaEventRecord(rt->ev_in, caller));
+  EET_CHECK_CUDA(cudaStreamWaitEvent(st, rt->ev_in, 0));
+
+  std::vector<int> pads(batch);
+  int t = 0;
+  for (int b = 0; b < batch; ++b) t = std::max(t, h_lengths[b]);
+  EET_REQUIRE(t == max_len, EET_ERR_ARG, "max_len must equal the longest prompt");
+  for (int b = 0; b < batch; ++b) {
+    EET_REQUIRE(h_lengths[b] >= 1, EET_ERR_ARG, "every prompt must have at least one token");
+    pads[b] = t - h_lengths[b];
+  }
+  // inputs go host -> pinned staging -> device (async DMA)
+  std::memcpy(rt->h_prompts, h_prompts, sizeof(int) * (size_t)batch * max_len);
+  EET_CHECK_CUDA(cudaMemcpyAsync(rt->d_prompts, rt->h_prompts, sizeof(int) * (size_t)batch * max_len,
+                                 cudaMemcpyHostToDevice, st));
+  const int h = rt->h;
+  const long long x_sb = (long long)m->max_prompt * h;
+
+  // prompt pass (PROMPT_PARALLEL over all slots at once)
+  StepPlan& pp = rt->plans[1];
+  plan_fill(pp, batch, t, pads.data(), t, EET_PHASE_PROMPT, st);
+  launch_embed_prompt(rt->dtype, m->tok_emb, m->pos_emb, rt->d_prompts, max_len, pp.pads,
+                      m->hidden, x_sb, batch, t, h, st);
+  for (int l = 0; l < m->layers; ++l)
+    layer_impl(rt, pp, m->hidden, x_sb, h, &m->layer[l], m->kcache[l], m->vcache[l], nullptr, 0,
+               true, t, st);
+
+  Claim tok(rt->pool, sizeof(long long) * (size_t)batch * std::max(steps, 1), EET_SCOPE_ACROSS,
+            "output.tokens");
+  if (steps > 0) {
+    int zero = 0;
+    EET_CHECK_CUDA(cudaMemcpyAsync(rt->d_filled, &t, sizeof(int), cudaMemcpyHostToDevice, st));
+    EET_CHECK_CUDA(cudaMemcpyAsync(rt->d_step, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+    StepPlan& ps = rt->plans[2];
+    plan_fill(ps, batch, 1, pads.data(), t, EET_PHASE_INCREMENTAL, st);
+    head_step(rt, m, m->hidden, x_sb, t - 1, batch, steps, tok.as<long long>(), d_logits, st);
+    // step 0 eagerly (settles every pool buffer), the rest replay one graph
+    decode_iteration(rt, m, batch, steps, tok.as<long long>(), d_logits, t + 1, st);
+    if (steps > 1) {
+      if (use_graph) {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        const uint64_t before = g_launches.load();
+        EET_CHECK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        try {
+          decode_iteration(rt, m, batch, steps, tok.as<long long>(), d_logits, -1, st);
+        } catch (...) {
+          cudaStreamEndCapture(st, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        EET_CHECK_CUDA(cudaStreamEndCapture(st, &g));
+        // captured launches run only when the graph replays: count them there
+        const uint64_t nodes = g_launches.load() - before;
+        g_launches.fetch_sub(nodes);
+        EET_CHECK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        for (int s = 1; s < steps; ++s) {
+          EET_CHECK_CUDA(cudaGraphLaunch(ge, st));
+          count_launch(nodes);
+        }
+        EET_CHECK_CUDA(cudaGraphExecDestroy(ge));
+        EET_CHECK_CUDA(cudaGraphDestroy(g));
+      } else {
+        for (int s = 1; s < steps; ++s)
+          decode_iteration(rt, m, batch, steps, tok.as<long long>(), d_logits, t + s + 1, st);
+      }
+    }
+    EET_CHECK_CUDA(cudaMemcpyAsync(rt->h_tokens, tok.ptr, sizeof(long long) * (size_t)batch * steps,
+                                   cudaMemcpyDeviceToHost, st));
+  }
+  tok.release();
+  EET_CHECK_CUDA(cudaEventRecord(rt->ev_out, st));
+  EET_CHECK_CUDA(cudaStreamWaitEvent(caller, rt->ev_out, 0));
+  EET_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (steps > 0) std::memcpy(h_tokens, rt->h_tokens, sizeof(long long) * (size_t)batch * steps);
+  EET_API_END
+}
+
+}  // extern "C"

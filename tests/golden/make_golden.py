@@ -214,15 +214,16 @@ def plumbing_cases():
             scope = "within" if rng.random() < 0.5 else "across"
             h = pool.request(size, scope=scope, tag="t")
             dec = pool.log.records[-1].decision
-            traces.append((len(traces), size, scope == "within", h.capacity, dec == "reuse"))
+            # (step, size, within?, granted capacity, reused?, buffer index)
+            traces.append((len(traces), size, scope == "within", h.capacity, dec == "reuse", h._index))
             live.append(h)
             if rng.random() < 0.6:
                 victim = live.pop(int(rng.integers(0, len(live))))
                 victim.release()
-                traces.append((len(traces), -1, 0, victim.capacity, 0))
-        traces.append((len(traces), 0, 0, 0, 0))   # trace separator
+                traces.append((len(traces), -1, 0, victim.capacity, 0, victim._index))
+        traces.append((len(traces), 0, 0, 0, 0, 0))   # trace separator
         traces.append((len(traces), pool.stats()["total_capacity"], pool.stats()["peak_in_use"],
-                       pool.stats()["malloc_count"], pool.stats()["reuse_count"]))
+                       pool.stats()["malloc_count"], pool.stats()["reuse_count"], 0))
     d["pool_traces"] = np.asarray(traces, np.int64)
     mb = mf.make_batch([5, 2, 4, 10])
     d["make_batch_5_2_4_10"] = np.asarray(mb.padding_len, np.int64)
