@@ -365,7 +365,7 @@ def main():
     roofline, kernels = None, {}
     if not args.no_profile and rank == 0:
         _lib.profile_enable(True)
-        step(graph=False) if kind == "generate" else step()
+        step(graph=True)
         torch.cuda.synchronize()
         summ = _lib.profile_summary()
         _lib.profile_enable(False)
@@ -389,7 +389,8 @@ def main():
                     "frac": round(ach / (hbm if hbm_k else tflops), 4), "traffic": traffic,
                     "algorithmic_per_launch": (by if hbm_k else fl) / n,
                     "avg_launch_us": kms / n * 1e3, "peak_source": peak_src,
-                    "timing": "profiled eager replay of one step, CUDA events per launch"}
+                    "timing": "profiled replay of one step: CUDA events around every launch on its "
+                              "stream (event-record nodes inside the decode graph)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -378,13 +378,15 @@ int decode_splits(int batch, int heads, int smax) {
 template <typename T, int E, int LPK, bool VEC>
 static void decode_launch(const DecodeArgs& a, cudaStream_t st) {
   dim3 grid(a.splits, a.heads, a.batch);
-  // algorithmic bytes: K and V rows of the window [pad_b, L) + q + out
-  double keys = 0;
-  for (int b = 0; b < a.batch; ++b)
-    keys += (a.L_host >= 0 ? a.L_host : a.smax) - (a.h_pads ? a.h_pads[b] : 0);
+  // algorithmic bytes: K and V rows of the window [pad_b, L) + q + out;
+  // inside a captured graph L is device-side: the profiler scales per key
   const double es = (double)sizeof(T);
-  ProfScope ps(K_ATTN_DECODE, st, keys * a.heads * a.hd * 2 * es + 2.0 * a.batch * a.heads * a.hd * es,
-               keys * a.heads * 4.0 * a.hd);
+  const double per_key_b = (double)a.heads * a.hd * 2 * es, per_key_f = (double)a.heads * 4.0 * a.hd;
+  double keys = 0;
+  if (a.L_host >= 0)
+    for (int b = 0; b < a.batch; ++b) keys += a.L_host - (a.h_pads ? a.h_pads[b] : 0);
+  ProfScope ps(K_ATTN_DECODE, st, keys * per_key_b + 2.0 * a.batch * a.heads * a.hd * es,
+               keys * per_key_f, a.L_host >= 0 ? 0.0 : per_key_b, a.L_host >= 0 ? 0.0 : per_key_f);
   attn_decode_kernel<T, E, LPK, VEC><<<grid, DWARPS * 32, 0, st>>>(a);
   EET_LAUNCH_CHECK();
 }

@@ -27,10 +27,20 @@ enum KernelKind : int {
 };
 struct ProfScope {
   int slot = -1;
+  bool graph = false;
   cudaStream_t st;
-  ProfScope(int kind, cudaStream_t st, double bytes, double flops);
+  // bytes/flops: fixed part; *_per_key: scaled by the attended key count of
+  // the replay when the launch sits in a captured decode graph (keys unknown
+  // at capture time), see prof_after_replay()
+  ProfScope(int kind, cudaStream_t st, double bytes, double flops, double bytes_per_key = 0,
+            double flops_per_key = 0);
   ~ProfScope();
 };
+bool prof_on();
+// after a graph replay: sync `st`, fold the captured launches in (keys = the
+// replay's attended keys summed over the batch)
+void prof_after_replay(cudaStream_t st, double keys);
+void prof_graph_reset();
 
 struct Fail {
   int code;
@@ -118,6 +128,8 @@ void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M,
 void gemv_small_m(int dtype, const void* A, int lda, const void* B, int ldb,
                   int M, int N, int K, const Epi& e, cudaStream_t st);
 void gemm_tc_sm100(int dtype, const void* A, int lda, const void* B, int ldb,
+                   int M, int N, int K, const Epi& e, cudaStream_t st);
+void gemv_tc_sm100(int dtype, const void* A, int lda, const void* B, int ldb,
                    int M, int N, int K, const Epi& e, cudaStream_t st);
 // Dispatch by dtype and M (the one GEMM entry the runtime uses).
 void gemm(int dtype, const void* A, int lda, const void* B, int ldb, int M,

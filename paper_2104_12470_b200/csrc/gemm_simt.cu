@@ -217,9 +217,9 @@ void gemv_small_m(int dtype, const void* A, int lda, const void* B, int ldb, int
   }
 }
 
-// The GEMM entry the runtime uses: fp32 mode -> FFMA kernels; 16-bit modes ->
-// tcgen05 tensor cores (TMA-fed), with the HBM-bound small-M case on the
-// streaming GEMV.
+// The GEMM entry the runtime uses: fp32 mode -> FFMA kernels (GEMV for the
+// decode rows); 16-bit modes -> tcgen05 tensor cores fed by TMA: the tiled
+// persistent GEMM for prompt passes, the swap-AB split-K GEMV for decode.
 static bool tc_eligible(const void* A, int lda, const void* B, int ldb, int K) {
   return (K % 8 == 0) && (lda % 8 == 0) && (ldb % 8 == 0) &&
          ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
@@ -228,16 +228,14 @@ static bool tc_eligible(const void* A, int lda, const void* B, int ldb, int K) {
 void gemm(int dtype, const void* A, int lda, const void* B, int ldb, int M, int N, int K,
           const Epi& e, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
-  if (M <= 16) {
-    gemv_small_m(dtype, A, lda, B, ldb, M, N, K, e, st);
-    return;
-  }
   if (dtype == EET_F32) {
-    gemm_f32_simt((const float*)A, lda, (const float*)B, ldb, M, N, K, e, st);
+    M <= 16 ? gemv_small_m(dtype, A, lda, B, ldb, M, N, K, e, st)
+            : gemm_f32_simt((const float*)A, lda, (const float*)B, ldb, M, N, K, e, st);
     return;
   }
   if (tc_eligible(A, lda, B, ldb, K)) {
-    gemm_tc_sm100(dtype, A, lda, B, ldb, M, N, K, e, st);
+    M <= 32 ? gemv_tc_sm100(dtype, A, lda, B, ldb, M, N, K, e, st)     // decode: swap-AB split-K
+            : gemm_tc_sm100(dtype, A, lda, B, ldb, M, N, K, e, st);
     return;
   }
   // 16-bit operands whose rows are not 16-byte aligned (tiny hidden sizes in

@@ -22,40 +22,78 @@ namespace {
 struct ProfRec {
   int kind;
   cudaEvent_t ev0, ev1;
-  double bytes, flops;
+  double bytes, flops, bytes_per_key, flops_per_key;
+};
+struct ProfAcc {
+  uint64_t n = 0;
+  double ms = 0, bytes = 0, flops = 0;
 };
 struct Profiler {
   bool on = false;
-  std::vector<ProfRec> recs;
+  std::vector<ProfRec> eager, graph;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
   size_t used = 0;
+  ProfAcc acc[K_KIND_COUNT];
+  std::pair<cudaEvent_t, cudaEvent_t> events() {
+    if (used == spare.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      spare.push_back({a, b});
+    }
+    return spare[used++];
+  }
 } g_prof;
 
 const char* kKindNames[K_KIND_COUNT] = {"layernorm", "softmax", "embed", "argmax", "advance",
                                         "gemm_f32", "gemv", "gemm_tc", "attn_prefill",
                                         "attn_decode"};
+
+void fold(const ProfRec& r, double keys) {
+  float e = 0.f;
+  EET_CHECK_CUDA(cudaEventElapsedTime(&e, r.ev0, r.ev1));
+  ProfAcc& a = g_prof.acc[r.kind];
+  a.n += 1;
+  a.ms += e;
+  a.bytes += r.bytes + r.bytes_per_key * keys;
+  a.flops += r.flops + r.flops_per_key * keys;
+}
 }  // namespace
 
-ProfScope::ProfScope(int kind, cudaStream_t s, double bytes, double flops) : st(s) {
+bool prof_on() { return g_prof.on; }
+
+ProfScope::ProfScope(int kind, cudaStream_t s, double bytes, double flops, double bpk, double fpk)
+    : st(s) {
   count_launch();
   if (!g_prof.on) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
-  if (g_prof.used == g_prof.spare.size()) {
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    g_prof.spare.push_back({a, b});
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return;
+  auto ev = g_prof.events();
+  graph = cs == cudaStreamCaptureStatusActive;
+  if (graph) {   // an event-record node inside the captured graph
+    cudaEventRecordWithFlags(ev.first, st, cudaEventRecordExternal);
+    slot = (int)g_prof.graph.size();
+    g_prof.graph.push_back(ProfRec{kind, ev.first, ev.second, bytes, flops, bpk, fpk});
+  } else {
+    cudaEventRecord(ev.first, st);
+    slot = (int)g_prof.eager.size();
+    g_prof.eager.push_back(ProfRec{kind, ev.first, ev.second, bytes, flops, 0, 0});
   }
-  auto ev = g_prof.spare[g_prof.used++];
-  cudaEventRecord(ev.first, st);
-  slot = (int)g_prof.recs.size();
-  g_prof.recs.push_back(ProfRec{kind, ev.first, ev.second, bytes, flops});
 }
 
 ProfScope::~ProfScope() {
-  if (slot >= 0) cudaEventRecord(g_prof.recs[slot].ev1, st);
+  if (slot < 0) return;
+  if (graph) cudaEventRecordWithFlags(g_prof.graph[slot].ev1, st, cudaEventRecordExternal);
+  else cudaEventRecord(g_prof.eager[slot].ev1, st);
 }
+
+void prof_after_replay(cudaStream_t st, double keys) {
+  if (!g_prof.on || g_prof.graph.empty()) return;
+  EET_CHECK_CUDA(cudaStreamSynchronize(st));
+  for (const auto& r : g_prof.graph) fold(r, keys);
+}
+
+void prof_graph_reset() { g_prof.graph.clear(); }
 
 }  // namespace eet
 
@@ -85,8 +123,10 @@ int eet_profile_enable(int on) {
   EET_API_BEGIN
   EET_CHECK_CUDA(cudaDeviceSynchronize());
   g_prof.on = on != 0;
-  g_prof.recs.clear();
+  g_prof.eager.clear();
+  g_prof.graph.clear();
   g_prof.used = 0;
+  for (auto& a : g_prof.acc) a = ProfAcc{};
   EET_API_END
 }
 
@@ -99,22 +139,15 @@ const char* eet_profile_kind_name(int kind) {
 int eet_profile_summary(int kind, uint64_t* count, double* total_ms, double* bytes,
                         double* flops) {
   EET_API_BEGIN
+  EET_REQUIRE(kind >= 0 && kind < K_KIND_COUNT, EET_ERR_ARG, "bad kernel kind");
   EET_CHECK_CUDA(cudaDeviceSynchronize());
-  uint64_t n = 0;
-  double ms = 0, by = 0, fl = 0;
-  for (const auto& r : g_prof.recs) {
-    if (r.kind != kind) continue;
-    float e = 0.f;
-    EET_CHECK_CUDA(cudaEventElapsedTime(&e, r.ev0, r.ev1));
-    ++n;
-    ms += e;
-    by += r.bytes;
-    fl += r.flops;
-  }
-  *count = n;
-  *total_ms = ms;
-  *bytes = by;
-  *flops = fl;
+  for (const auto& r : g_prof.eager) fold(r, 0);   // resolve pending eager launches
+  g_prof.eager.clear();
+  const ProfAcc& a = g_prof.acc[kind];
+  *count = a.n;
+  *total_ms = a.ms;
+  *bytes = a.bytes;
+  *flops = a.flops;
   EET_API_END
 }
 
@@ -749,7 +782,13 @@ int eet_generate(eet_runtime* rt, const eet_model* m, const int* h_prompts, cons
         for (int s = 1; s < steps; ++s) {
           EET_CHECK_CUDA(cudaGraphLaunch(ge, st));
           count_launch(nodes);
+          if (prof_on()) {                 // keys attended by this replay
+            double keys = 0;
+            for (int b = 0; b < batch; ++b) keys += t + s + 1 - pads[b];
+            prof_after_replay(st, keys);
+          }
         }
+        prof_graph_reset();
         EET_CHECK_CUDA(cudaGraphExecDestroy(ge));
         EET_CHECK_CUDA(cudaGraphDestroy(g));
       } else {

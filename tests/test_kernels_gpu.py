@@ -172,10 +172,12 @@ def test_fp32_gemm_exact_path(eet, M, N, K):
 @pytest.mark.parametrize("dt", [1, 2])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 384, 192), (1000, 768, 200),
                                    (4096, 3 * 2048, 2048), (257, 128, 4096), (130, 50257, 1024),
-                                   (33, 1000, 8), (5, 3072, 1024)])
+                                   (33, 1000, 8), (5, 3072, 1024), (16, 4096, 1024),
+                                   (1, 50257, 1024), (24, 1024, 4096), (32, 3072, 1024),
+                                   (3, 1000, 200), (2, 130, 64)])
 def test_tensor_core_gemm(eet, dt, M, N, K):
-    """tcgen05 GEMM (M > 16) / streaming GEMV (M <= 16) vs fp64 on the same
-    16-bit-rounded operands: only accumulation-order error is allowed."""
+    """tcgen05 GEMM (M > 32) / tcgen05 swap-AB split-K GEMV (M <= 32) vs fp64
+    on the same 16-bit-rounded operands: only accumulation-order error."""
     rng = np.random.default_rng(M + N + K)
     a = rng.normal(size=(M, K)).astype(np.float32)
     b = rng.normal(size=(N, K)).astype(np.float32)
