@@ -9,7 +9,7 @@
 //  * attn_decode_kernel  — incremental phase: split-K flash-decoding over the
 //    KV cache, one query per sequence; the last CTA of each (b, head) merges
 //    the splits. HBM-bound on the K/V read.
-#include "common.cuh"
+#include "sm100.cuh"
 
 namespace eet {
 
@@ -197,6 +197,7 @@ void launch_attn_prefill(const PrefillArgs& a, cudaStream_t st) {
   const double es = (double)dtype_size(a.dtype);
   const double bytes = rows * a.heads * a.hd * es * 4;
   const double flops = pairs * a.heads * 4.0 * a.hd;
+  if (attn_prefill_tc(a, a.q_rows, st, bytes, flops)) return;   // tcgen05 path (16-bit, hd 64/128)
   switch (a.dtype) {
     case EET_F32: prefill_dispatch<float>(a, st, bytes, flops); break;
     case EET_BF16: prefill_dispatch<__nv_bfloat16>(a, st, bytes, flops); break;
@@ -215,9 +216,12 @@ constexpr int DWARPS = 4;
 template <typename T, int E, int LPK, bool VEC>
 __global__ void __launch_bounds__(DWARPS * 32) attn_decode_kernel(DecodeArgs a) {
   constexpr int G = 32 / LPK;
+  constexpr int U = 8;                    // key steps whose K/V loads are in flight together
   __shared__ float sm_m[DWARPS], sm_l[DWARPS];
   __shared__ float sm_acc[DWARPS][LPK * E];
   __shared__ int sm_last;
+  sm100::griddep_wait();                  // K/V of this step were written by the QKV GEMV
+  sm100::griddep_launch_dependents();
   const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / LPK, sub = lane % LPK;
@@ -251,44 +255,49 @@ __global__ void __launch_bounds__(DWARPS * 32) attn_decode_kernel(DecodeArgs a) 
 #pragma unroll
   for (int e = 0; e < E; ++e) acc[e] = 0.f;
 
-  for (int jb = ks + warp * G; jb < ke; jb += DWARPS * G) {   // warp-uniform trip count
-    const int j = jb + g;
-    const bool ok = j < ke;
-    float kv[E], vv[E];
+  auto load_row = [&](const T* src, int j, float* dst) {
     const long long off = (long long)j * hd + d0;
-    if (ok && d0 < hd) {
-      if constexpr (VEC) {
+    if constexpr (VEC) {
 #pragma unroll
-        for (int c = 0; c < E; c += 16 / (int)sizeof(T)) {
-          load16<T>(Kc + off + c, kv + c);
-          load16<T>(Vc + off + c, vv + c);
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          bool in = d0 + e < hd;
-          kv[e] = in ? to_f(Kc[off + e]) : 0.f;
-          vv[e] = in ? to_f(Vc[off + e]) : 0.f;
-        }
-      }
+      for (int c = 0; c < E; c += 16 / (int)sizeof(T)) load16<T>(src + off + c, dst + c);
     } else {
 #pragma unroll
-      for (int e = 0; e < E; ++e) kv[e] = vv[e] = 0.f;
+      for (int e = 0; e < E; ++e) dst[e] = (d0 + e < hd) ? to_f(src[off + e]) : 0.f;
     }
-    float dot = 0.f;
+  };
+
+  constexpr int STEP = DWARPS * G;        // keys per CTA-wide step
+  for (int jb = ks + warp * G; jb < ke; jb += STEP * U) {   // warp-uniform trip count
+    float kv[U][E], vv[U][E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) dot = fmaf(q[e], kv[e], dot);
+    for (int u = 0; u < U; ++u) {         // issue every load of the batch first
+      const int j = jb + u * STEP + g;
+      if (j < ke && d0 < hd) {
+        load_row(Kc, j, kv[u]);
+        load_row(Vc, j, vv[u]);
+      } else {
 #pragma unroll
-    for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    if (ok) {
-      const float s = dot * a.scale;
-      const float mn = fmaxf(m, s);
-      const float corr = (m == -INFINITY) ? 0.f : expf(m - mn);
-      const float p = expf(s - mn);
-      l = l * corr + p;
+        for (int e = 0; e < E; ++e) kv[u][e] = vv[u][e] = 0.f;
+      }
+    }
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = fmaf(p, vv[e], acc[e] * corr);
-      m = mn;
+    for (int u = 0; u < U; ++u) {
+      const int j = jb + u * STEP + g;
+      float dot = 0.f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) dot = fmaf(q[e], kv[u][e], dot);
+#pragma unroll
+      for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (j < ke) {
+        const float s = dot * a.scale;
+        const float mn = fmaxf(m, s);
+        const float corr = (m == -INFINITY) ? 0.f : expf(m - mn);
+        const float p = expf(s - mn);
+        l = l * corr + p;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = fmaf(p, vv[u][e], acc[e] * corr);
+        m = mn;
+      }
     }
   }
   // merge the key groups of this warp (lanes with equal `sub`)
@@ -368,11 +377,14 @@ __global__ void __launch_bounds__(DWARPS * 32) attn_decode_kernel(DecodeArgs a) 
   if (threadIdx.x == 0) a.counters[b * a.heads + head] = 0;
 }
 
+// Splits per (b, head): ~128 keys per CTA (32 per warp = one batch of
+// in-flight loads) and at least ~2 CTAs per SM for small batches.
 int decode_splits(int batch, int heads, int smax) {
-  int pairs = std::max(1, batch * heads);
-  int want = (4 * 148 + pairs - 1) / pairs;          // ~4 CTAs per SM
-  int cap = std::max(1, (smax + 31) / 32);           // >= 32 keys per split
-  return std::max(1, std::min(want, std::min(cap, 64)));
+  const int pairs = std::max(1, batch * heads);
+  const int by_len = (smax + 127) / 128;
+  const int by_sms = (2 * 148 + pairs - 1) / pairs;
+  const int cap = std::max(1, (smax + 31) / 32);       // >= 32 keys per split
+  return std::max(1, std::min(std::max(by_len, by_sms), std::min(cap, 64)));
 }
 
 template <typename T, int E, int LPK, bool VEC>
@@ -387,7 +399,7 @@ static void decode_launch(const DecodeArgs& a, cudaStream_t st) {
     for (int b = 0; b < a.batch; ++b) keys += a.L_host - (a.h_pads ? a.h_pads[b] : 0);
   ProfScope ps(K_ATTN_DECODE, st, keys * per_key_b + 2.0 * a.batch * a.heads * a.hd * es,
                keys * per_key_f, a.L_host >= 0 ? 0.0 : per_key_b, a.L_host >= 0 ? 0.0 : per_key_f);
-  attn_decode_kernel<T, E, LPK, VEC><<<grid, DWARPS * 32, 0, st>>>(a);
+  launch_ex(attn_decode_kernel<T, E, LPK, VEC>, grid, dim3(DWARPS * 32), 0, st, true, dim3(1, 1, 1), a);
   EET_LAUNCH_CHECK();
 }
 

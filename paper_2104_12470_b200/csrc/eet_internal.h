@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <string>
 #include <atomic>
+#include <utility>
 
 #include "../../include/eet_b200.h"
 
@@ -148,8 +149,10 @@ struct PrefillArgs {
   float scale;
   int causal;
   int zero_pad_rows;   // padded layout: write zero rows for pad queries
+  int q_rows;          // rows of the packed q buffer (TMA extent)
 };
 void launch_attn_prefill(const PrefillArgs& a, cudaStream_t st);
+bool attn_prefill_tc(const PrefillArgs& a, int q_rows, cudaStream_t st, double bytes, double flops);
 
 struct DecodeArgs {
   int dtype;
@@ -169,6 +172,36 @@ struct DecodeArgs {
 };
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
 int decode_splits(int batch, int heads, int smax);
+
+// cudaLaunchKernelEx with optional programmatic-dependent-launch edge and
+// cluster shape. Kernels launched with pdl=true must execute
+// griddepcontrol.wait before touching memory written by earlier kernels.
+template <typename... KArgs, typename... Args>
+inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      bool pdl, dim3 cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  int n = 0;
+  if (pdl) {
+    attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster.x * cluster.y * cluster.z > 1) {
+    attrs[n].id = cudaLaunchAttributeClusterDimension;
+    attrs[n].val.clusterDim.x = cluster.x;
+    attrs[n].val.clusterDim.y = cluster.y;
+    attrs[n].val.clusterDim.z = cluster.z;
+    ++n;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = n;
+  EET_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // dtype helpers
 inline size_t dtype_size(int dt) { return dt == EET_F32 ? 4 : 2; }

@@ -11,10 +11,15 @@
 // Each CTA (128 threads) streams a K-range of one 128-row weight block
 // through a TMA ring (16 KB W + 2-4 KB X per 64-wide k-block), one lane
 // issues tcgen05.mma kind::f16 M=128 N=MN into TMEM, and all four warps read
-// the accumulator back (TMEM lane = weight row). K is split across CTAs to
-// put ~2 CTAs on every SM; partial sums go to a workspace and the last CTA of
-// each row block adds them in split order (deterministic) and runs the fused
-// epilogue (bias / GELU / residual / KV-cache scatter / logits).
+// the accumulator back (TMEM lane = weight row). K is split across the CTAs
+// of a thread-block cluster (<= 8) so ~2 CTAs land on every SM; the partial
+// tiles are summed through distributed shared memory in split order
+// (deterministic, no global round trip), each CTA finishing a slice of the
+// fused epilogue (bias / GELU / residual / KV-cache scatter / logits).
+//
+// Launched with programmatic dependent launch: weights are static, so the
+// first ring stages of W are requested before griddepcontrol.wait and
+// stream in while the previous kernel is still finishing.
 #include "sm100.cuh"
 
 namespace eet {
@@ -24,27 +29,27 @@ using namespace sm100;
 constexpr int ROWS = 128, BK = 64, THREADS = 128, STAGES = 4;
 constexpr int W_BYTES = ROWS * BK * 2;
 
-template <int MN> struct Cfg {
-  static constexpr int X_BYTES = MN * BK * 2;               // 2 KB (16) / 4 KB (32)
-  static constexpr int SMEM = STAGES * (W_BYTES + X_BYTES) + 1024 + 128;
+template <int MN> struct Lay {
+  static constexpr int X_BYTES = MN * BK * 2;
+  static constexpr int RED_OFF = STAGES * (W_BYTES + X_BYTES);
+  static constexpr int SMEM = RED_OFF + ROWS * MN * 4 + 1024 + 128;
 };
 
 template <typename T, int MN>
 __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
     const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
-    int N, int K, int kb_per_split, int splits, float* __restrict__ ws, int* __restrict__ counters,
-    Epi e) {
-  using C = Cfg<MN>;
+    int N, int K, int kb_per_split, int splits, Epi e) {
+  using L = Lay<MN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sW = smem;                                   // STAGES x 16 KB (1024-aligned)
   uint8_t* sX = smem + STAGES * W_BYTES;                // STAGES x X_BYTES
-  uint64_t* full = reinterpret_cast<uint64_t*>(sX + STAGES * C::X_BYTES);
+  float* red = reinterpret_cast<float*>(smem + L::RED_OFF);        // [MN][128] partial tile
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::RED_OFF + ROWS * MN * 4);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  __shared__ int s_last;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = blockIdx.x, split = blockIdx.y;
@@ -69,34 +74,47 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0 && lane == 0) {
-    // weights are read exactly once per step: stream them past L2
-    const uint64_t pol_w = 0x12F0000000000000ull;   // EVICT_FIRST
-    const uint64_t pol_x = 0x14F0000000000000ull;   // EVICT_LAST (re-read by every CTA)
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int kb = kb0; kb < kb1; ++kb) {
+    const uint64_t pol_w = 0x12F0000000000000ull;   // EVICT_FIRST: weights read once per step
+    const uint64_t pol_x = 0x14F0000000000000ull;   // EVICT_LAST: X re-read by every CTA
+    // weights are static: fill the ring before waiting on the previous grid
+    const int pre = min(STAGES, kb1 - kb0);
+    for (int i = 0; i < pre; ++i) {
+      mbar_expect_tx(&full[i], W_BYTES + L::X_BYTES);
+      tma_load_2d(sW + i * W_BYTES, &mapW, &full[i], (kb0 + i) * BK, rb * ROWS, pol_w);
+    }
+    griddep_wait();
+    griddep_launch_dependents();
+    for (int i = 0; i < pre; ++i)
+      tma_load_2d(sX + i * L::X_BYTES, &mapX, &full[i], (kb0 + i) * BK, 0, pol_x);
+    int stage = pre % STAGES;
+    uint32_t phase = pre == STAGES ? 1 : 0;
+    for (int kb = kb0 + pre; kb < kb1; ++kb) {
       mbar_wait(&empty[stage], phase ^ 1);
-      mbar_expect_tx(&full[stage], W_BYTES + C::X_BYTES);
+      mbar_expect_tx(&full[stage], W_BYTES + L::X_BYTES);
       tma_load_2d(sW + stage * W_BYTES, &mapW, &full[stage], kb * BK, rb * ROWS, pol_w);
-      tma_load_2d(sX + stage * C::X_BYTES, &mapX, &full[stage], kb * BK, 0, pol_x);
+      tma_load_2d(sX + stage * L::X_BYTES, &mapX, &full[stage], kb * BK, 0, pol_x);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
-  } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t idesc = instr_desc(std::is_same<T, __nv_bfloat16>::value ? 1 : 0, ROWS, MN);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int kb = kb0; kb < kb1; ++kb) {
-      mbar_wait(&full[stage], phase);
-      tc_fence_after();
-      const uint32_t w0 = smem_u32(sW + stage * W_BYTES);
-      const uint32_t x0 = smem_u32(sX + stage * C::X_BYTES);
+  } else {
+    griddep_wait();
+    griddep_launch_dependents();
+    if (warp == 1 && lane == 0) {
+      constexpr uint32_t idesc = instr_desc(std::is_same<T, __nv_bfloat16>::value ? 1 : 0, ROWS, MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t w0 = smem_u32(sW + stage * W_BYTES);
+        const uint32_t x0 = smem_u32(sX + stage * L::X_BYTES);
 #pragma unroll
-      for (int k = 0; k < BK / 16; ++k)
-        mma_f16(tmem, smem_desc(w0 + k * 32), smem_desc(x0 + k * 32), idesc, (kb > kb0) | k);
-      mma_commit(&empty[stage]);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        for (int k = 0; k < BK / 16; ++k)
+          mma_f16(tmem, smem_desc(w0 + k * 32), smem_desc(x0 + k * 32), idesc, (kb > kb0) | k);
+        mma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      mma_commit(done);
     }
-    mma_commit(done);
   }
   __syncwarp();
   mbar_wait(done, 0);
@@ -104,7 +122,7 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
 
   // accumulator row = this thread's weight row; columns = token rows
   const int row = warp * 32 + lane;
-  const int n = rb * ROWS + row;
+  const int n0 = rb * ROWS;
   float acc[MN];
   {
     uint32_t r[MN];
@@ -118,82 +136,53 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   if (warp == 1) tmem_dealloc(tmem, 32);
 
   if (splits == 1) {
-    if (n < N)
+    if (n0 + row < N)
 #pragma unroll
       for (int m = 0; m < MN; ++m)
-        if (m < M) epi_apply<T>(e, m, n, acc[m]);
+        if (m < M) epi_apply<T>(e, m, n0 + row, acc[m]);
     return;
   }
-  // publish this split's partial tile, then the last split reduces in order
-  float* mine = ws + (((size_t)rb * splits + split) * ROWS + row) * MN;
+  // split-K reduction through distributed shared memory: publish the
+  // partial tile transposed ([m][row]), then every CTA of the cluster sums
+  // a contiguous slice over the splits in rank order and finishes it.
 #pragma unroll
-  for (int m = 0; m < MN; m += 4)
-    __stcg(reinterpret_cast<float4*>(mine + m), make_float4(acc[m], acc[m + 1], acc[m + 2], acc[m + 3]));
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&counters[rb], 1) == splits - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-#pragma unroll
-  for (int m = 0; m < MN; ++m) acc[m] = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float* src = ws + (((size_t)rb * splits + s) * ROWS + row) * MN;
-#pragma unroll
-    for (int m = 0; m < MN; m += 4) {
-      float4 v = __ldcg(reinterpret_cast<const float4*>(src + m));
-      acc[m] += v.x; acc[m + 1] += v.y; acc[m + 2] += v.z; acc[m + 3] += v.w;
-    }
+  for (int m = 0; m < MN; ++m) red[m * ROWS + row] = acc[m];
+  cluster_sync();
+  const int total = M * ROWS;
+  const int chunk = (total + splits - 1) / splits;
+  const int lo = (int)cluster_ctarank() * chunk, hi = min(total, lo + chunk);
+  const uint32_t red0 = smem_u32(red);
+  for (int idx = lo + threadIdx.x; idx < hi; idx += THREADS) {
+    const uint32_t off = red0 + idx * 4;
+    float v = 0.f;
+    for (int p = 0; p < splits; ++p) v += dsmem_ld(dsmem_addr(off, p));
+    const int m = idx / ROWS, n = n0 + idx % ROWS;
+    if (n < N) epi_apply<T>(e, m, n, v);
   }
-  if (n < N)
-#pragma unroll
-    for (int m = 0; m < MN; ++m)
-      if (m < M) epi_apply<T>(e, m, n, acc[m]);
-  if (threadIdx.x == 0) counters[rb] = 0;
-}
-
-// Grow-only split-K scratch (allocated outside graph capture: the eager
-// warm-up step of every shape reaches here before any capture does).
-static float* g_ws = nullptr;
-static size_t g_ws_bytes = 0;
-static int* g_cnt = nullptr;
-static size_t g_cnt_n = 0;
-
-static void ensure_scratch(size_t ws_bytes, size_t counters) {
-  if (ws_bytes > g_ws_bytes) {
-    if (g_ws) cudaFree(g_ws);
-    EET_CHECK_CUDA(cudaMalloc(&g_ws, ws_bytes));
-    g_ws_bytes = ws_bytes;
-  }
-  if (counters > g_cnt_n) {
-    if (g_cnt) cudaFree(g_cnt);
-    EET_CHECK_CUDA(cudaMalloc(&g_cnt, counters * sizeof(int)));
-    EET_CHECK_CUDA(cudaMemset(g_cnt, 0, counters * sizeof(int)));
-    g_cnt_n = counters;
-  }
+  cluster_sync();                       // peers may still be reading our slice
 }
 
 template <typename T, int MN>
 static void launch(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
                    const Epi& e, int dtype, cudaStream_t st) {
-  using C = Cfg<MN>;
+  using L = Lay<MN>;
   const int rbs = (N + ROWS - 1) / ROWS;
   const int nkb = (K + BK - 1) / BK;
   const int target = 2 * device_sm_count();
-  int splits = std::min(std::max(1, (target + rbs - 1) / rbs), std::min(nkb, 16));
+  int splits = std::min(std::max(1, (target + rbs - 1) / rbs), std::min(nkb, 8));
   const int kbps = (nkb + splits - 1) / splits;
   splits = (nkb + kbps - 1) / kbps;
-  if (splits > 1) ensure_scratch((size_t)rbs * splits * ROWS * MN * sizeof(float), (size_t)rbs);
   CUtensorMap mw = make_tma_map_2d(B, N, K, ldb, ROWS, dtype);
   CUtensorMap mx = make_tma_map_2d(A, M, K, lda, MN, dtype);
   auto kern = gemv_tc_kernel<T, MN>;
   static bool attr = false;
   if (!attr) {
-    EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
     attr = true;
   }
   ProfScope ps(K_GEMV, st, gemm_bytes(M, N, K, 2, e), 2.0 * M * N * K);
-  kern<<<dim3(rbs, splits), THREADS, C::SMEM, st>>>(mw, mx, M, N, K, kbps, splits, g_ws, g_cnt, e);
+  launch_ex(kern, dim3(rbs, splits), dim3(THREADS), L::SMEM, st, true, dim3(1, splits, 1), mw, mx, M,
+            N, K, kbps, splits, e);
   EET_LAUNCH_CHECK();
 }
 

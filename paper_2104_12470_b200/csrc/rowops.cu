@@ -5,7 +5,7 @@
 // into t = 2^k sub-blocks of `threads` lanes; lane `tid` of the CTA owns items
 // sb*threads + tid for sb < t (folding.py:57-70 map_index). One launch shape
 // therefore covers h up to 16384 and seq up to 4096 with <= 1024 threads.
-#include "common.cuh"
+#include "sm100.cuh"
 
 namespace eet {
 
@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(1024) ln_kernel(
     const float* __restrict__ b, TO* __restrict__ y, int ldy, int h,
     int sub_blocks, int lanes) {
   __shared__ float red[32];
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
   const int r = blockIdx.x;
   const float* xr;
   if (rinfo) {
@@ -92,8 +94,8 @@ static void ln_dispatch(const float* x, long long x_sb, long long x_ss, const in
 #define LN_CASE(T_)                                                                      \
   if (p.sub_blocks <= T_) {                                                              \
     ProfScope ps(K_LAYERNORM, st, (double)rows * h * (4 + sizeof(TO)) + 8.0 * h, 8.0 * rows * h); \
-    ln_kernel<TO, VEC, T_><<<rows, threads, 0, st>>>(x, x_sb, x_ss, rinfo, g, b, y, ldy, h, \
-                                                    p.sub_blocks, p.threads);            \
+    launch_ex(ln_kernel<TO, VEC, T_>, dim3(rows), dim3(threads), 0, st, true, dim3(1, 1, 1), x,   \
+              x_sb, x_ss, rinfo, g, b, y, ldy, h, p.sub_blocks, p.threads);              \
     EET_LAUNCH_CHECK();                                                                  \
     return;                                                                              \
   }
@@ -247,6 +249,8 @@ __global__ void embed_step_kernel(const T* __restrict__ tok, const T* __restrict
                                   const int* __restrict__ cur, const int* __restrict__ pads,
                                   const int* __restrict__ d_filled, float* __restrict__ x,
                                   long long x_sb, int h) {
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
   const int b = blockIdx.x;
   const int p = *d_filled - pads[b];
   const T* tr = tok + (long long)cur[b] * h;
@@ -275,12 +279,13 @@ void launch_embed_step(int dtype, const void* tok, const void* pos, const int* c
                        int h, cudaStream_t st) {
   int threads = std::min(256, round32(h));
   ProfScope ps(K_EMBED, st, (double)batch * h * (4 + 2 * dtype_size(dtype)), 1.0 * batch * h);
+  const dim3 one(1, 1, 1);
   if (dtype == EET_F32)
-    embed_step_kernel<float><<<batch, threads, 0, st>>>((const float*)tok, (const float*)pos, cur, pads, d_filled, x, x_sb, h);
+    launch_ex(embed_step_kernel<float>, dim3(batch), dim3(threads), 0, st, true, one, (const float*)tok, (const float*)pos, cur, pads, d_filled, x, x_sb, h);
   else if (dtype == EET_BF16)
-    embed_step_kernel<__nv_bfloat16><<<batch, threads, 0, st>>>((const __nv_bfloat16*)tok, (const __nv_bfloat16*)pos, cur, pads, d_filled, x, x_sb, h);
+    launch_ex(embed_step_kernel<__nv_bfloat16>, dim3(batch), dim3(threads), 0, st, true, one, (const __nv_bfloat16*)tok, (const __nv_bfloat16*)pos, cur, pads, d_filled, x, x_sb, h);
   else
-    embed_step_kernel<__half><<<batch, threads, 0, st>>>((const __half*)tok, (const __half*)pos, cur, pads, d_filled, x, x_sb, h);
+    launch_ex(embed_step_kernel<__half>, dim3(batch), dim3(threads), 0, st, true, one, (const __half*)tok, (const __half*)pos, cur, pads, d_filled, x, x_sb, h);
   EET_LAUNCH_CHECK();
 }
 
@@ -293,6 +298,8 @@ __global__ void __launch_bounds__(1024) argmax_kernel(
     float* __restrict__ logits_all, int batch) {
   __shared__ float sv[32];
   __shared__ int si[32];
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
   const int b = blockIdx.x;
   const float* row = logits + (long long)b * vocab;
   const int step = d_step ? *d_step : 0;
@@ -333,19 +340,21 @@ __global__ void __launch_bounds__(1024) argmax_kernel(
 void launch_argmax(const float* logits, int batch, int vocab, int* cur, long long* toks,
                    int steps, const int* d_step, float* logits_all, cudaStream_t st) {
   ProfScope ps(K_ARGMAX, st, 4.0 * batch * vocab * (logits_all ? 2 : 1), 1.0 * batch * vocab);
-  argmax_kernel<<<batch, 1024, 0, st>>>(logits, vocab, cur, toks, steps, d_step, logits_all,
-                                        batch);
+  launch_ex(argmax_kernel, dim3(batch), dim3(1024), 0, st, true, dim3(1, 1, 1), logits, vocab, cur,
+            toks, steps, d_step, logits_all, batch);
   EET_LAUNCH_CHECK();
 }
 
 __global__ void advance_kernel(int* d_filled, int* d_step) {
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
   *d_filled += 1;
   *d_step += 1;
 }
 
 void launch_advance(int* d_filled, int* d_step, cudaStream_t st) {
   ProfScope ps(K_ADVANCE, st, 16.0, 2.0);
-  advance_kernel<<<1, 1, 0, st>>>(d_filled, d_step);
+  launch_ex(advance_kernel, dim3(1), dim3(1), 0, st, true, dim3(1, 1, 1), d_filled, d_step);
   EET_LAUNCH_CHECK();
 }
 

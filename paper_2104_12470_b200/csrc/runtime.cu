@@ -540,6 +540,7 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
     a.scale = scale;
     a.causal = causal ? 1 : 0;
     a.zero_pad_rows = 0;
+    a.q_rows = p.T;
     launch_attn_prefill(a, st);
   } else {
     DecodeArgs a{};
