@@ -171,7 +171,7 @@ struct DecodeArgs {
   int splits;
 };
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
-int decode_splits(int batch, int heads, int smax);
+int decode_splits(int batch, int heads, int smax, int hd, int es);
 
 // cudaLaunchKernelEx with optional programmatic-dependent-launch edge and
 // cluster shape. Kernels launched with pdl=true must execute

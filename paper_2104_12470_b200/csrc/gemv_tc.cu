@@ -151,11 +151,16 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   const int total = M * ROWS;
   const int chunk = (total + splits - 1) / splits;
   const int lo = (int)cluster_ctarank() * chunk, hi = min(total, lo + chunk);
-  const uint32_t red0 = smem_u32(red);
+  const float* peer[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) peer[p] = map_peer(red, p < splits ? p : 0);
   for (int idx = lo + threadIdx.x; idx < hi; idx += THREADS) {
-    const uint32_t off = red0 + idx * 4;
+    float part[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) part[p] = p < splits ? peer[p][idx] : 0.f;   // all in flight
     float v = 0.f;
-    for (int p = 0; p < splits; ++p) v += dsmem_ld(dsmem_addr(off, p));
+#pragma unroll
+    for (int p = 0; p < 8; ++p) v += part[p];                                 // rank order
     const int m = idx / ROWS, n = n0 + idx % ROWS;
     if (n < N) epi_apply<T>(e, m, n, v);
   }

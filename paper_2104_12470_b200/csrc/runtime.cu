@@ -612,7 +612,7 @@ int eet_runtime_create(eet_runtime** out, int dtype, int hidden, int heads, int 
   rt->bmax = max_batch;
   rt->smax = max_sequence;
   rt->pool = pool;
-  rt->splits = decode_splits(max_batch, heads, max_sequence);
+  rt->splits = decode_splits(max_batch, heads, max_sequence, hidden / heads, (int)dtype_size(dtype));
   for (auto& p : rt->plans) plan_alloc(rt.get(), p);
   rt->part = (float*)rt->dev(sizeof(float) * (size_t)max_batch * heads * rt->splits * (rt->hd + 2));
   rt->counters = (int*)rt->dev(sizeof(int) * (size_t)max_batch * heads);

@@ -126,6 +126,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 1-D bulk copy global -> shared (TMA engine), completion on an mbarrier
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---- programmatic dependent launch (PDL)
 // wait: block until the preceding grid in the stream has completed and its
 // writes are visible (no-op when launched without a programmatic edge).
@@ -152,6 +161,14 @@ __device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
   return r;
+}
+// generic pointer to the same object in cluster CTA `rank` (plain loads,
+// freely scheduled by the compiler)
+template <typename P>
+__device__ __forceinline__ P* map_peer(P* p, uint32_t rank) {
+  uint64_t r;
+  asm("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(p)), "r"(rank));
+  return reinterpret_cast<P*>(r);
 }
 __device__ __forceinline__ float dsmem_ld(uint32_t addr) {
   float v;

@@ -102,8 +102,6 @@ def main():
                 out[f"layer_{name}_{k}"] = {"launches": n, "us_per_launch": round(ms / n * 1e3, 2),
                                             "GB/s": round(by / (ms / 1e3) / 1e9, 1),
                                             "TFLOP/s": round(fl / (ms / 1e3) / 1e12, 2)}
-        for k, v in list(out.items()):
-            pass
     for k, v in out.items():
         print(k, json.dumps(v), flush=True)
 
