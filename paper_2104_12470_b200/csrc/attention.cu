@@ -378,17 +378,18 @@ __global__ void __launch_bounds__(DWARPS * 32) attn_decode_kernel(DecodeArgs a) 
 }
 
 // Streaming variant: the split's K and V rows are contiguous in the
-// [b, heads, s_max, hd] cache, so one thread moves them into shared memory
-// with TMA bulk copies, 64 keys per mbarrier-tracked chunk; warps start on
-// chunk 0 while the rest are in flight. Requires 16-byte rows.
+// [b, heads, s_max, hd] cache, so a producer warp moves them into a
+// two-chunk shared-memory ring with TMA bulk copies (64 keys per chunk,
+// full/empty mbarriers) while the four compute warps consume the other
+// chunk. 32 KB of ring per CTA (hd 64, 16-bit) keeps ~7 CTAs per SM, one
+// wave for the c2 decode step. Requires 16-byte key rows.
 constexpr int DCHUNK = 64;
-constexpr int DMAX_CHUNKS = 8;
 
 template <typename T, int E, int LPK>
-__global__ void __launch_bounds__(DWARPS * 32) attn_decode_bulk_kernel(DecodeArgs a, int max_keys) {
+__global__ void __launch_bounds__((DWARPS + 1) * 32) attn_decode_bulk_kernel(DecodeArgs a) {
   constexpr int G = 32 / LPK;
   extern __shared__ __align__(128) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t bars[DMAX_CHUNKS];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
   __shared__ float sm_m[DWARPS], sm_l[DWARPS];
   __shared__ float sm_acc[DWARPS][LPK * E];
   __shared__ int sm_last;
@@ -396,10 +397,13 @@ __global__ void __launch_bounds__(DWARPS * 32) attn_decode_bulk_kernel(DecodeArg
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / LPK, sub = lane % LPK;
   const int hd = a.hd;
-  T* sK = reinterpret_cast<T*>(dsm);
-  T* sV = sK + (size_t)max_keys * hd;
+  const size_t chunk_elems = (size_t)DCHUNK * hd;
+  T* ring = reinterpret_cast<T*>(dsm);                    // [2][K chunk | V chunk]
   if (threadIdx.x == 0) {
-    for (int c = 0; c < DMAX_CHUNKS; ++c) sm100::mbar_init(&bars[c], 1);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], DWARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -408,88 +412,100 @@ __global__ void __launch_bounds__(DWARPS * 32) attn_decode_bulk_kernel(DecodeArg
   const int pad = a.pads[b];
   const int L = (a.kv_start ? *a.kv_start : 0) + a.kv_base + 1;
   const int n = L - pad;
-  const int chunk = (n + a.splits - 1) / a.splits;
-  const int ks = pad + split * chunk, ke = min(ks + chunk, L);
+  const int per = (n + a.splits - 1) / a.splits;
+  const int ks = pad + split * per, ke = min(ks + per, L);
   const int nk = max(ke - ks, 0);
   const int nch = (nk + DCHUNK - 1) / DCHUNK;
   const long long base = ((long long)b * a.heads + head) * a.smax * hd;
-  const T* Kc = reinterpret_cast<const T*>(a.kc) + base + (long long)ks * hd;
-  const T* Vc = reinterpret_cast<const T*>(a.vc) + base + (long long)ks * hd;
-  if (threadIdx.x == 0) {
+
+  if (warp == DWARPS) {                   // ---- producer warp
+    if (lane == 0) {
+      const T* Kc = reinterpret_cast<const T*>(a.kc) + base + (long long)ks * hd;
+      const T* Vc = reinterpret_cast<const T*>(a.vc) + base + (long long)ks * hd;
+      for (int c = 0; c < nch; ++c) {
+        const int buf = c & 1;
+        if (c >= 2) sm100::mbar_wait(&empty[buf], ((c >> 1) - 1) & 1);
+        const int kn = min(DCHUNK, nk - c * DCHUNK);
+        const uint32_t bytes = (uint32_t)(kn * hd * sizeof(T));
+        T* dst = ring + buf * 2 * chunk_elems;
+        sm100::mbar_expect_tx(&full[buf], 2 * bytes);
+        sm100::bulk_load(dst, Kc + (size_t)c * chunk_elems, bytes, &full[buf]);
+        sm100::bulk_load(dst + chunk_elems, Vc + (size_t)c * chunk_elems, bytes, &full[buf]);
+      }
+    }
+  } else {                                // ---- compute warps
+    const T* Q = reinterpret_cast<const T*>(a.q) + (long long)b * a.ldq + head * hd;
+    const int d0 = sub * E;
+    float q[E];
+    if (d0 < hd) {
+#pragma unroll
+      for (int c = 0; c < E; c += 16 / (int)sizeof(T)) load16<T>(Q + d0 + c, q + c);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) q[e] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f, acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.f;
     for (int c = 0; c < nch; ++c) {
-      const int k0 = c * DCHUNK, kn = min(DCHUNK, nk - k0);
-      const uint32_t bytes = (uint32_t)(kn * hd * sizeof(T));
-      sm100::mbar_expect_tx(&bars[c], 2 * bytes);
-      sm100::bulk_load(sK + (size_t)k0 * hd, Kc + (size_t)k0 * hd, bytes, &bars[c]);
-      sm100::bulk_load(sV + (size_t)k0 * hd, Vc + (size_t)k0 * hd, bytes, &bars[c]);
-    }
-  }
-  const T* Q = reinterpret_cast<const T*>(a.q) + (long long)b * a.ldq + head * hd;
-  const int d0 = sub * E;
-  float q[E];
-  if (d0 < hd) {
+      const int buf = c & 1;
+      sm100::mbar_wait(&full[buf], (c >> 1) & 1);
+      const T* sK = ring + buf * 2 * chunk_elems;
+      const T* sV = sK + chunk_elems;
+      const int kn = min(DCHUNK, nk - c * DCHUNK);
+      for (int jb = warp * G; jb < kn; jb += DWARPS * G) {     // warp-uniform
+        const int j = jb + g;
+        const bool ok = j < kn;
+        float kv[E], vv[E];
+        if (ok && d0 < hd) {
 #pragma unroll
-    for (int c = 0; c < E; c += 16 / (int)sizeof(T)) load16<T>(Q + d0 + c, q + c);
-  } else {
+          for (int cc = 0; cc < E; cc += 16 / (int)sizeof(T)) {
+            load16<T>(sK + (size_t)j * hd + d0 + cc, kv + cc);
+            load16<T>(sV + (size_t)j * hd + d0 + cc, vv + cc);
+          }
+        } else {
 #pragma unroll
-    for (int e = 0; e < E; ++e) q[e] = 0.f;
-  }
-  float m = -INFINITY, l = 0.f, acc[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.f;
-  for (int c = 0; c < nch; ++c) {
-    sm100::mbar_wait(&bars[c], 0);
-    const int k0 = c * DCHUNK, k1 = min(nk, k0 + DCHUNK);
-    for (int jb = k0 + warp * G; jb < k1; jb += DWARPS * G) {   // warp-uniform
-      const int j = jb + g;
-      const bool ok = j < k1;
-      float kv[E], vv[E];
-      if (ok && d0 < hd) {
-#pragma unroll
-        for (int cc = 0; cc < E; cc += 16 / (int)sizeof(T)) {
-          load16<T>(sK + (size_t)j * hd + d0 + cc, kv + cc);
-          load16<T>(sV + (size_t)j * hd + d0 + cc, vv + cc);
+          for (int e = 0; e < E; ++e) kv[e] = vv[e] = 0.f;
         }
-      } else {
+        float dot = 0.f;
 #pragma unroll
-        for (int e = 0; e < E; ++e) kv[e] = vv[e] = 0.f;
+        for (int e = 0; e < E; ++e) dot = fmaf(q[e], kv[e], dot);
+#pragma unroll
+        for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (ok) {
+          const float s = dot * a.scale;
+          const float mn = fmaxf(m, s);
+          const float corr = (m == -INFINITY) ? 0.f : expf(m - mn);
+          const float p = expf(s - mn);
+          l = l * corr + p;
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[e] = fmaf(p, vv[e], acc[e] * corr);
+          m = mn;
+        }
       }
-      float dot = 0.f;
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&empty[buf]);
+    }
 #pragma unroll
-      for (int e = 0; e < E; ++e) dot = fmaf(q[e], kv[e], dot);
+    for (int o = LPK; o < 32; o <<= 1) {
+      float mo = __shfl_xor_sync(0xffffffffu, m, o);
+      float lo = __shfl_xor_sync(0xffffffffu, l, o);
+      float mn = fmaxf(m, mo);
+      float c1 = (m == -INFINITY) ? 0.f : expf(m - mn);
+      float c2 = (mo == -INFINITY) ? 0.f : expf(mo - mn);
 #pragma unroll
-      for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (ok) {
-        const float s = dot * a.scale;
-        const float mn = fmaxf(m, s);
-        const float corr = (m == -INFINITY) ? 0.f : expf(m - mn);
-        const float p = expf(s - mn);
-        l = l * corr + p;
-#pragma unroll
-        for (int e = 0; e < E; ++e) acc[e] = fmaf(p, vv[e], acc[e] * corr);
-        m = mn;
+      for (int e = 0; e < E; ++e) {
+        float ao = __shfl_xor_sync(0xffffffffu, acc[e], o);
+        acc[e] = acc[e] * c1 + ao * c2;
       }
+      l = l * c1 + lo * c2;
+      m = mn;
     }
-  }
+    if (g == 0) {
+      if (sub == 0) { sm_m[warp] = m; sm_l[warp] = l; }
 #pragma unroll
-  for (int o = LPK; o < 32; o <<= 1) {
-    float mo = __shfl_xor_sync(0xffffffffu, m, o);
-    float lo = __shfl_xor_sync(0xffffffffu, l, o);
-    float mn = fmaxf(m, mo);
-    float c1 = (m == -INFINITY) ? 0.f : expf(m - mn);
-    float c2 = (mo == -INFINITY) ? 0.f : expf(mo - mn);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      float ao = __shfl_xor_sync(0xffffffffu, acc[e], o);
-      acc[e] = acc[e] * c1 + ao * c2;
+      for (int e = 0; e < E; ++e) sm_acc[warp][d0 + e] = acc[e];
     }
-    l = l * c1 + lo * c2;
-    m = mn;
-  }
-  if (g == 0) {
-    if (sub == 0) { sm_m[warp] = m; sm_l[warp] = l; }
-#pragma unroll
-    for (int e = 0; e < E; ++e) sm_acc[warp][d0 + e] = acc[e];
   }
   __syncthreads();
   float* part = a.part + (((long long)b * a.heads + head) * a.splits + split) * (hd + 2);
@@ -538,14 +554,12 @@ __global__ void __launch_bounds__(DWARPS * 32) attn_decode_bulk_kernel(DecodeArg
   if (threadIdx.x == 0) a.counters[b * a.heads + head] = 0;
 }
 
-// Largest per-split key count the streaming kernel holds in shared memory.
-static int bulk_max_keys(int hd, int es) { return std::min(DMAX_CHUNKS * DCHUNK, (96 * 1024) / (2 * hd * es)); }
-
 // Splits per (b, head): ~128 keys per CTA (32 per warp = one batch of
 // in-flight loads) and at least ~2 CTAs per SM for small batches.
 int decode_splits(int batch, int heads, int smax, int hd, int es) {
+  (void)hd; (void)es;
   const int pairs = std::max(1, batch * heads);
-  const int by_len = std::max((smax + 255) / 256, (smax + bulk_max_keys(hd, es) - 1) / bulk_max_keys(hd, es));
+  const int by_len = (smax + 255) / 256;
   const int by_sms = (2 * 148 + pairs - 1) / pairs;
   const int cap = std::max(1, (smax + 31) / 32);       // >= 32 keys per split
   return std::max(1, std::min(std::max(by_len, by_sms), std::min(cap, 64)));
@@ -568,7 +582,7 @@ static void decode_launch(const DecodeArgs& a, cudaStream_t st) {
 }
 
 template <typename T, int E, int LPK>
-static void decode_bulk_launch(const DecodeArgs& a, cudaStream_t st, int max_keys) {
+static void decode_bulk_launch(const DecodeArgs& a, cudaStream_t st) {
   dim3 grid(a.splits, a.heads, a.batch);
   double keys = 0;
   for (int b = 0; b < a.batch; ++b)
@@ -576,12 +590,12 @@ static void decode_bulk_launch(const DecodeArgs& a, cudaStream_t st, int max_key
   const double es = (double)sizeof(T);
   const double per_key_b = (double)a.heads * a.hd * 2 * es, per_key_f = (double)a.heads * 4.0 * a.hd;
   if (a.L_host < 0) keys = 0;
-  const size_t smem = (size_t)2 * max_keys * a.hd * sizeof(T);
+  const size_t smem = (size_t)2 * 2 * DCHUNK * a.hd * sizeof(T);
   auto kern = attn_decode_bulk_kernel<T, E, LPK>;
   EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfScope ps(K_ATTN_DECODE, st, keys * per_key_b + 2.0 * a.batch * a.heads * a.hd * es,
                keys * per_key_f, a.L_host >= 0 ? 0.0 : per_key_b, a.L_host >= 0 ? 0.0 : per_key_f);
-  launch_ex(kern, grid, dim3(DWARPS * 32), smem, st, true, dim3(1, 1, 1), a, max_keys);
+  launch_ex(kern, grid, dim3((DWARPS + 1) * 32), smem, st, true, dim3(1, 1, 1), a);
   EET_LAUNCH_CHECK();
 }
 
@@ -590,20 +604,19 @@ static void decode_dispatch(const DecodeArgs& a, cudaStream_t st) {
   constexpr int VE = 16 / sizeof(T);
   const int hd = a.hd;
   {
-    // streaming kernel: 16-byte rows, the split's keys fit in shared memory
-    const int max_keys = (a.smax + a.splits - 1) / a.splits;
+    // streaming kernel: 16-byte key rows
     const bool ok = (hd * (int)sizeof(T)) % 16 == 0 && hd % VE == 0 && hd / VE <= 32 &&
-                    max_keys <= bulk_max_keys(hd, sizeof(T)) && (a.ldq % VE) == 0 &&
+                    hd * (int)sizeof(T) <= 512 && (a.ldq % VE) == 0 &&
                     ((reinterpret_cast<uintptr_t>(a.kc) | reinterpret_cast<uintptr_t>(a.vc) |
                       reinterpret_cast<uintptr_t>(a.q)) & 15) == 0;
     if (ok) {
       const int lanes = hd / VE;
-      if (lanes <= 1) return decode_bulk_launch<T, VE, 1>(a, st, max_keys);
-      if (lanes <= 2) return decode_bulk_launch<T, VE, 2>(a, st, max_keys);
-      if (lanes <= 4) return decode_bulk_launch<T, VE, 4>(a, st, max_keys);
-      if (lanes <= 8) return decode_bulk_launch<T, VE, 8>(a, st, max_keys);
-      if (lanes <= 16) return decode_bulk_launch<T, VE, 16>(a, st, max_keys);
-      return decode_bulk_launch<T, VE, 32>(a, st, max_keys);
+      if (lanes <= 1) return decode_bulk_launch<T, VE, 1>(a, st);
+      if (lanes <= 2) return decode_bulk_launch<T, VE, 2>(a, st);
+      if (lanes <= 4) return decode_bulk_launch<T, VE, 4>(a, st);
+      if (lanes <= 8) return decode_bulk_launch<T, VE, 8>(a, st);
+      if (lanes <= 16) return decode_bulk_launch<T, VE, 16>(a, st);
+      return decode_bulk_launch<T, VE, 32>(a, st);
     }
   }
   EET_REQUIRE(hd <= 256, EET_ERR_UNSUPPORTED, "decode attention: head_dim > 256");

@@ -132,6 +132,11 @@ void gemm_tc_sm100(int dtype, const void* A, int lda, const void* B, int ldb,
                    int M, int N, int K, const Epi& e, cudaStream_t st);
 void gemv_tc_sm100(int dtype, const void* A, int lda, const void* B, int ldb,
                    int M, int N, int K, const Epi& e, cudaStream_t st);
+// decode GEMV with the LayerNorm of its input rows fused into the prologue;
+// false when the shape is not eligible (caller runs LN + gemm instead)
+bool gemv_tc_ln_sm100(int dtype, const float* x, long long x_sb, long long x_ss,
+                      const int2* rinfo, const float* g, const float* b, const void* B,
+                      int ldb, int M, int N, int K, const Epi& e, cudaStream_t st);
 // Dispatch by dtype and M (the one GEMM entry the runtime uses).
 void gemm(int dtype, const void* A, int lda, const void* B, int ldb, int M,
           int N, int K, const Epi& e, cudaStream_t st);

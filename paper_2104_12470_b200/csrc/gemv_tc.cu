@@ -9,13 +9,19 @@
 //   D[n (128 weight rows), m (token)] += W[n, k:k+64] . X[m, k:k+64]^T
 //
 // Each CTA (128 threads) streams a K-range of one 128-row weight block
-// through a TMA ring (16 KB W + 2-4 KB X per 64-wide k-block), one lane
-// issues tcgen05.mma kind::f16 M=128 N=MN into TMEM, and all four warps read
-// the accumulator back (TMEM lane = weight row). K is split across the CTAs
-// of a thread-block cluster (<= 8) so ~2 CTAs land on every SM; the partial
-// tiles are summed through distributed shared memory in split order
+// through a TMA ring (16 KB per 64-wide k-block), one lane issues
+// tcgen05.mma kind::f16 M=128 N=MN into TMEM, and all four warps read the
+// accumulator back (TMEM lane = weight row). K is split across the CTAs of a
+// thread-block cluster (<= 8) so ~2 CTAs land on every SM; the partial tiles
+// are summed through distributed shared memory in split order
 // (deterministic, no global round trip), each CTA finishing a slice of the
 // fused epilogue (bias / GELU / residual / KV-cache scatter / logits).
+//
+// X comes either from a 16-bit activation buffer (TMA) or — LNX — straight
+// from the fp32 residual stream: the CTA normalises its token rows
+// (runtime.py:83-94, single-pass statistics) for its own K-range and writes
+// them into the 128B-swizzled operand layout, so the decode step needs no
+// separate LayerNorm launch before QKV, W1 and the LM head.
 //
 // Launched with programmatic dependent launch: weights are static, so the
 // first ring stages of W are requested before griddepcontrol.wait and
@@ -26,36 +32,49 @@ namespace eet {
 namespace gv {
 using namespace sm100;
 
-constexpr int ROWS = 128, BK = 64, THREADS = 128, STAGES = 4;
+constexpr int ROWS = 128, BK = 64, THREADS = 128, STAGES = 4, MAX_KBPS = 16;
 constexpr int W_BYTES = ROWS * BK * 2;
 
-template <int MN> struct Lay {
-  static constexpr int X_BYTES = MN * BK * 2;
-  static constexpr int RED_OFF = STAGES * (W_BYTES + X_BYTES);
-  static constexpr int SMEM = RED_OFF + ROWS * MN * 4 + 1024 + 128;
+struct LnSrc {                      // LNX operand source
+  const float* x;                   // residual stream, row m at rinfo[m]
+  long long x_sb, x_ss;
+  const int2* rinfo;
+  const float* g;
+  const float* b;
 };
 
-template <typename T, int MN>
+template <int MN, bool LNX> struct Lay {
+  static constexpr int X_TILE = MN * BK * 2;                 // one [MN x 64] operand tile
+  static constexpr int X_TILES = LNX ? MAX_KBPS : STAGES;    // whole K-range vs TMA ring
+  static constexpr int X_OFF = STAGES * W_BYTES;
+  static constexpr int RED_OFF = X_OFF + X_TILES * X_TILE;
+  static constexpr int BAR_OFF = RED_OFF + ROWS * MN * 4;
+  static constexpr int SMEM = BAR_OFF + 128 + 1024;
+};
+
+template <typename T, int MN, bool LNX>
 __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
-    const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, int M,
-    int N, int K, int kb_per_split, int splits, Epi e) {
-  using L = Lay<MN>;
+    const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapX, LnSrc ln,
+    int M, int N, int K, int kb_per_split, int splits, Epi e) {
+  using L = Lay<MN, LNX>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sW = smem;                                   // STAGES x 16 KB (1024-aligned)
-  uint8_t* sX = smem + STAGES * W_BYTES;                // STAGES x X_BYTES
+  uint8_t* sX = smem + L::X_OFF;                        // X tiles (2-4 KB each, 1024-aligned)
   float* red = reinterpret_cast<float*>(smem + L::RED_OFF);        // [MN][128] partial tile
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::RED_OFF + ROWS * MN * 4);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* x_ready = done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_ready + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rb = blockIdx.x, split = blockIdx.y;
   const int nkb = (K + BK - 1) / BK;
   const int kb0 = split * kb_per_split;
   const int kb1 = min(nkb, kb0 + kb_per_split);
+  constexpr uint32_t STAGE_TX = LNX ? W_BYTES : W_BYTES + L::X_TILE;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -63,9 +82,10 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
+    mbar_init(x_ready, THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapW) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
+    if (!LNX) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapX) : "memory");
   }
   if (warp == 1) tmem_alloc(tmem_slot, 32);
   tc_fence_before();
@@ -73,48 +93,95 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  const uint64_t pol_w = 0x12F0000000000000ull;   // EVICT_FIRST: weights read once per step
+  const uint64_t pol_x = 0x14F0000000000000ull;   // EVICT_LAST: X re-read by every CTA
+  const int pre = min(STAGES, kb1 - kb0);
   if (warp == 0 && lane == 0) {
-    const uint64_t pol_w = 0x12F0000000000000ull;   // EVICT_FIRST: weights read once per step
-    const uint64_t pol_x = 0x14F0000000000000ull;   // EVICT_LAST: X re-read by every CTA
     // weights are static: fill the ring before waiting on the previous grid
-    const int pre = min(STAGES, kb1 - kb0);
     for (int i = 0; i < pre; ++i) {
-      mbar_expect_tx(&full[i], W_BYTES + L::X_BYTES);
+      mbar_expect_tx(&full[i], STAGE_TX);
       tma_load_2d(sW + i * W_BYTES, &mapW, &full[i], (kb0 + i) * BK, rb * ROWS, pol_w);
     }
-    griddep_wait();
-    griddep_launch_dependents();
-    for (int i = 0; i < pre; ++i)
-      tma_load_2d(sX + i * L::X_BYTES, &mapX, &full[i], (kb0 + i) * BK, 0, pol_x);
+  }
+  griddep_wait();
+  griddep_launch_dependents();
+
+  if constexpr (LNX) {
+    // ---- fused LayerNorm of the token rows into the swizzled X tiles
+    const int h = K;
+    const int c0 = kb0 * BK, ncols = (kb1 - kb0) * BK;
+    for (int m = warp; m < MN; m += THREADS / 32) {
+      float mean = 0.f, rstd = 0.f;
+      const float* xr = nullptr;
+      if (m < M) {
+        const int2 ri = ln.rinfo[m];
+        xr = ln.x + ri.x * ln.x_sb + ri.y * ln.x_ss;
+        float s = 0.f, ss = 0.f;
+        for (int c = lane * 4; c < h; c += 128) {
+          const float4 v = *reinterpret_cast<const float4*>(xr + c);
+          s += v.x + v.y + v.z + v.w;
+          ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        }
+        s = warp_sum(s);
+        ss = warp_sum(ss);
+        mean = s / (float)h;
+        rstd = 1.0f / sqrtf(fmaxf(ss / (float)h - mean * mean, 0.f) + 1e-5f);
+      }
+      // 8-column groups of this CTA's K range -> 16 B swizzled chunks
+      for (int grp = lane; grp < ncols / 8; grp += 32) {
+        const int col = c0 + grp * 8;
+        float y[8];
+        if (m < M && col < h) {
+          const float4 a = *reinterpret_cast<const float4*>(xr + col);
+          const float4 b = *reinterpret_cast<const float4*>(xr + col + 4);
+          const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) y[i] = (xv[i] - mean) * rstd * ln.g[col + i] + ln.b[col + i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) y[i] = 0.f;
+        }
+        const int tile = grp >> 3, chunk = grp & 7;
+        uint8_t* dst = sX + tile * L::X_TILE + (m >> 3) * 1024 + (m & 7) * 128 + ((chunk ^ (m & 7)) << 4);
+        store16<T>(reinterpret_cast<T*>(dst), y);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA
+    mbar_arrive(x_ready);
+  }
+
+  if (warp == 0 && lane == 0) {
+    if constexpr (!LNX) {
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(sX + i * L::X_TILE, &mapX, &full[i], (kb0 + i) * BK, 0, pol_x);
+    }
     int stage = pre % STAGES;
     uint32_t phase = pre == STAGES ? 1 : 0;
     for (int kb = kb0 + pre; kb < kb1; ++kb) {
       mbar_wait(&empty[stage], phase ^ 1);
-      mbar_expect_tx(&full[stage], W_BYTES + L::X_BYTES);
+      mbar_expect_tx(&full[stage], STAGE_TX);
       tma_load_2d(sW + stage * W_BYTES, &mapW, &full[stage], kb * BK, rb * ROWS, pol_w);
-      tma_load_2d(sX + stage * L::X_BYTES, &mapX, &full[stage], kb * BK, 0, pol_x);
+      if constexpr (!LNX)
+        tma_load_2d(sX + stage * L::X_TILE, &mapX, &full[stage], kb * BK, 0, pol_x);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
-  } else {
-    griddep_wait();
-    griddep_launch_dependents();
-    if (warp == 1 && lane == 0) {
-      constexpr uint32_t idesc = instr_desc(std::is_same<T, __nv_bfloat16>::value ? 1 : 0, ROWS, MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        const uint32_t w0 = smem_u32(sW + stage * W_BYTES);
-        const uint32_t x0 = smem_u32(sX + stage * L::X_BYTES);
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc = instr_desc(std::is_same<T, __nv_bfloat16>::value ? 1 : 0, ROWS, MN);
+    if constexpr (LNX) mbar_wait(x_ready, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      const uint32_t w0 = smem_u32(sW + stage * W_BYTES);
+      const uint32_t x0 = smem_u32(sX + (LNX ? (kb - kb0) : stage) * L::X_TILE);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          mma_f16(tmem, smem_desc(w0 + k * 32), smem_desc(x0 + k * 32), idesc, (kb > kb0) | k);
-        mma_commit(&empty[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-      }
-      mma_commit(done);
+      for (int k = 0; k < BK / 16; ++k)
+        mma_f16(tmem, smem_desc(w0 + k * 32), smem_desc(x0 + k * 32), idesc, (kb > kb0) | k);
+      mma_commit(&empty[stage]);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
+    mma_commit(done);
   }
   __syncwarp();
   mbar_wait(done, 0);
@@ -167,27 +234,38 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   cluster_sync();                       // peers may still be reading our slice
 }
 
-template <typename T, int MN>
-static void launch(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
-                   const Epi& e, int dtype, cudaStream_t st) {
-  using L = Lay<MN>;
+// splits: ~2 CTAs per SM, <= 8 per cluster, every split non-empty; LNX keeps
+// the whole K-range of a CTA in shared memory (<= MAX_KBPS k-blocks).
+static void plan_splits(int rbs, int nkb, bool lnx, int* splits, int* kbps) {
+  const int target = 2 * device_sm_count();
+  int s = std::min(std::max(1, (target + rbs - 1) / rbs), std::min(nkb, 8));
+  if (lnx) s = std::max(s, (nkb + MAX_KBPS - 1) / MAX_KBPS);
+  const int k = (nkb + s - 1) / s;
+  *kbps = k;
+  *splits = (nkb + k - 1) / k;
+}
+
+template <typename T, int MN, bool LNX>
+static void launch(const void* A, int lda, const LnSrc& ln, const void* B, int ldb, int M, int N,
+                   int K, const Epi& e, int dtype, cudaStream_t st) {
+  using L = Lay<MN, LNX>;
   const int rbs = (N + ROWS - 1) / ROWS;
   const int nkb = (K + BK - 1) / BK;
-  const int target = 2 * device_sm_count();
-  int splits = std::min(std::max(1, (target + rbs - 1) / rbs), std::min(nkb, 8));
-  const int kbps = (nkb + splits - 1) / splits;
-  splits = (nkb + kbps - 1) / kbps;
+  int splits, kbps;
+  plan_splits(rbs, nkb, LNX, &splits, &kbps);
+  EET_REQUIRE(splits <= 8, EET_ERR_UNSUPPORTED, "gemv_tc: K too long for one cluster");
   CUtensorMap mw = make_tma_map_2d(B, N, K, ldb, ROWS, dtype);
-  CUtensorMap mx = make_tma_map_2d(A, M, K, lda, MN, dtype);
-  auto kern = gemv_tc_kernel<T, MN>;
+  CUtensorMap mx = LNX ? mw : make_tma_map_2d(A, M, K, lda, MN, dtype);
+  auto kern = gemv_tc_kernel<T, MN, LNX>;
   static bool attr = false;
   if (!attr) {
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
     attr = true;
   }
-  ProfScope ps(K_GEMV, st, gemm_bytes(M, N, K, 2, e), 2.0 * M * N * K);
-  launch_ex(kern, dim3(rbs, splits), dim3(THREADS), L::SMEM, st, true, dim3(1, splits, 1), mw, mx, M,
-            N, K, kbps, splits, e);
+  const double xbytes = LNX ? (double)M * K * 4 : (double)M * K * 2;
+  ProfScope ps(K_GEMV, st, gemm_bytes(M, N, K, 2, e) - (double)M * K * 2 + xbytes, 2.0 * M * N * K);
+  launch_ex(kern, dim3(rbs, splits), dim3(THREADS), L::SMEM, st, true, dim3(1, splits, 1), mw, mx,
+            ln, M, N, K, kbps, splits, e);
   EET_LAUNCH_CHECK();
 }
 
@@ -197,13 +275,34 @@ void gemv_tc_sm100(int dtype, const void* A, int lda, const void* B, int ldb, in
                    const Epi& e, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
   EET_REQUIRE(M <= 32, EET_ERR_ARG, "gemv_tc: more than 32 token rows");
+  const gv::LnSrc none{};
   if (dtype == EET_BF16) {
-    M <= 16 ? gv::launch<__nv_bfloat16, 16>(A, lda, B, ldb, M, N, K, e, dtype, st)
-            : gv::launch<__nv_bfloat16, 32>(A, lda, B, ldb, M, N, K, e, dtype, st);
+    M <= 16 ? gv::launch<__nv_bfloat16, 16, false>(A, lda, none, B, ldb, M, N, K, e, dtype, st)
+            : gv::launch<__nv_bfloat16, 32, false>(A, lda, none, B, ldb, M, N, K, e, dtype, st);
   } else {
-    M <= 16 ? gv::launch<__half, 16>(A, lda, B, ldb, M, N, K, e, dtype, st)
-            : gv::launch<__half, 32>(A, lda, B, ldb, M, N, K, e, dtype, st);
+    M <= 16 ? gv::launch<__half, 16, false>(A, lda, none, B, ldb, M, N, K, e, dtype, st)
+            : gv::launch<__half, 32, false>(A, lda, none, B, ldb, M, N, K, e, dtype, st);
   }
+}
+
+// LayerNorm-fused variant: X = LN(x[rows]) * g + b computed in the prologue.
+// Returns false (caller runs LN + GEMV separately) when the shape does not fit.
+bool gemv_tc_ln_sm100(int dtype, const float* x, long long x_sb, long long x_ss,
+                      const int2* rinfo, const float* g, const float* b, const void* B, int ldb,
+                      int M, int N, int K, const Epi& e, cudaStream_t st) {
+  if (dtype == EET_F32 || M <= 0 || M > 32 || K % 64 != 0 || ldb % 8 != 0 ||
+      (reinterpret_cast<uintptr_t>(x) & 15) || (x_sb & 3) || (x_ss & 3) ||
+      (reinterpret_cast<uintptr_t>(B) & 15) || (K / 64 + gv::MAX_KBPS - 1) / gv::MAX_KBPS > 8)
+    return false;
+  const gv::LnSrc ln{x, x_sb, x_ss, rinfo, g, b};
+  if (dtype == EET_BF16) {
+    M <= 16 ? gv::launch<__nv_bfloat16, 16, true>(nullptr, 0, ln, B, ldb, M, N, K, e, dtype, st)
+            : gv::launch<__nv_bfloat16, 32, true>(nullptr, 0, ln, B, ldb, M, N, K, e, dtype, st);
+  } else {
+    M <= 16 ? gv::launch<__half, 16, true>(nullptr, 0, ln, B, ldb, M, N, K, e, dtype, st)
+            : gv::launch<__half, 32, true>(nullptr, 0, ln, B, ldb, M, N, K, e, dtype, st);
+  }
+  return true;
 }
 
 }  // namespace eet

@@ -501,9 +501,6 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
   const int scope = (p.phase == EET_PHASE_PROMPT) ? EET_SCOPE_WITHIN : EET_SCOPE_ACROSS;
   if (T == 0) return;
 
-  Claim ln(rt->pool, (size_t)T * h * es, scope, "attention.layernorm");
-  launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln1_g, w->ln1_b, ln.ptr, dt, h, h, 0, st);
-
   Claim q(rt->pool, (size_t)T * h * es, scope, "attention.query");
   {
     Epi e;
@@ -519,9 +516,14 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
     e.smax = rt->smax;
     e.kv_start = kv_dev;
     e.kv_base = kv_base;
-    gemm(dt, ln.ptr, h, w->wqkv, h, T, 3 * h, h, e, st);
+    // decode rows: LN1 runs inside the GEMV prologue; otherwise LN -> GEMM
+    if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b, w->wqkv, h,
+                                      T, 3 * h, h, e, st))) {
+      Claim ln(rt->pool, (size_t)T * h * es, scope, "attention.layernorm");
+      launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln1_g, w->ln1_b, ln.ptr, dt, h, h, 0, st);
+      gemm(dt, ln.ptr, h, w->wqkv, h, T, 3 * h, h, e, st);
+    }
   }
-  ln.release();
 
   Claim ctx(rt->pool, (size_t)T * h * es, scope, "attention.context");
   const float scale = 1.0f / std::sqrt((float)rt->hd);
@@ -572,8 +574,6 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
   ctx.release();
 
   // feed-forward block: both requests use across-module scope (runtime.py:200-207)
-  Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
-  launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln2_g, w->ln2_b, ln2.ptr, dt, h, h, 0, st);
   Claim mid(rt->pool, (size_t)T * 4 * h * es, EET_SCOPE_ACROSS, "ffn.intermediate");
   {
     Epi e;
@@ -581,7 +581,12 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
     e.bias = w->b_1;
     e.out = mid.ptr;
     e.ldo = 4 * h;
-    gemm(dt, ln2.ptr, h, w->w1, h, T, 4 * h, h, e, st);
+    if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T,
+                                      4 * h, h, e, st))) {
+      Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
+      launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln2_g, w->ln2_b, ln2.ptr, dt, h, h, 0, st);
+      gemm(dt, ln2.ptr, h, w->w1, h, T, 4 * h, h, e, st);
+    }
   }
   {
     Epi e;
@@ -592,7 +597,6 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
     gemm(dt, mid.ptr, 4 * h, w->w2, 4 * h, T, h, 4 * h, e, st);
   }
   mid.release();
-  ln2.release();
 }
 
 extern "C" {
@@ -683,20 +687,22 @@ static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long 
                       cudaStream_t st) {
   const int h = rt->h, dt = rt->dtype;
   const size_t es = dtype_size(dt);
-  // rows (b, slot) of x; a tiny row map lives in plan 2's rinfo tail
-  Claim ln(rt->pool, (size_t)batch * h * es, EET_SCOPE_ACROSS, "output.layernorm");
   Claim lg(rt->pool, (size_t)batch * m->vocab * 4, EET_SCOPE_ACROSS, "output.logits");
-  launch_layer_norm(x + (long long)slot * h, x_sb, h, nullptr, batch, m->lnf_g, m->lnf_b, ln.ptr,
-                    dt, h, h, 0, st);
   Epi e;
   e.mode = EPI_STORE_F32;
   e.out = lg.ptr;
   e.ldo = m->vocab;
-  gemm(dt, ln.ptr, h, m->head, h, batch, m->vocab, h, e, st);
+  // rows (b, slot): the decode plan's row map (b, 0) over x shifted by `slot`
+  const float* xs = x + (long long)slot * h;
+  if (!(batch <= 32 && gemv_tc_ln_sm100(dt, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g, m->lnf_b,
+                                        m->head, h, batch, m->vocab, h, e, st))) {
+    Claim ln(rt->pool, (size_t)batch * h * es, EET_SCOPE_ACROSS, "output.layernorm");
+    launch_layer_norm(xs, x_sb, h, nullptr, batch, m->lnf_g, m->lnf_b, ln.ptr, dt, h, h, 0, st);
+    gemm(dt, ln.ptr, h, m->head, h, batch, m->vocab, h, e, st);
+  }
   launch_argmax(lg.as<float>(), batch, m->vocab, rt->d_cur, d_tokens, steps, rt->d_step, d_logits,
                 st);
   lg.release();
-  ln.release();
 }
 
 // L_host: keys attended this step when known on the host (-1 under capture)
