@@ -167,6 +167,31 @@ int eet_encoder_layer_forward(eet_runtime* rt, float* x, long long x_sb,
                               const eet_layer_weights* w, const int* h_pads,
                               void* stream);
 
+/* ------------------------------------------------------- tensor parallel
+ * Megatron split for h >= 4096: each rank holds heads/tp
+ * heads (wqkv [3*h/tp, h], wo [h, h/tp]) and 4h/tp FFN columns (w1
+ * [4h/tp, h], w2 [h, 4h/tp]); LN parameters and x are replicated. A layer is
+ *   p = attention_partial(x); all_reduce(p); residual_add(x, p);
+ *   p = ffn_partial(x);       all_reduce(p); residual_add(x, p);
+ * with the all-reduce (sum over ranks, fp32 [rows, h]) done by the caller's
+ * communicator (NCCL over NVLink). `rows` returns the packed valid-token
+ * count; partial must hold rows * h floats. The reference has no TP
+ * (PAPER.md:85); these stages are new. */
+int eet_runtime_create_tp(eet_runtime** out, int dtype, int hidden,
+                          int heads_total, int tp_rank, int tp_size,
+                          int max_batch, int max_sequence, eet_pool* pool);
+int eet_tp_attention_partial(eet_runtime* rt, const float* x, long long x_sb,
+                             long long x_ss, int batch, int t,
+                             const eet_layer_weights* w, void* kcache,
+                             void* vcache, int kv_filled, const int* h_pads,
+                             int seq_len, int phase, float* partial, int* rows,
+                             void* stream);
+int eet_tp_ffn_partial(eet_runtime* rt, const float* x, long long x_sb,
+                       long long x_ss, const eet_layer_weights* w,
+                       float* partial, void* stream);
+int eet_tp_residual_add(eet_runtime* rt, float* x, long long x_sb, long long x_ss,
+                        const float* reduced, void* stream);
+
 /* ------------------------------------------------------------- generation */
 typedef struct {
   int layers, vocab, max_sequence;

@@ -107,44 +107,55 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   griddep_launch_dependents();
 
   if constexpr (LNX) {
-    // ---- fused LayerNorm of the token rows into the swizzled X tiles
+    // ---- fused LayerNorm of the token rows into the swizzled X tiles.
+    // TPR threads per row, all rows at once: one pass of independent float4
+    // loads for the statistics, one for this CTA's columns.
+    constexpr int TPR = THREADS / MN;                   // 8 (MN 16) or 4 (MN 32)
     const int h = K;
+    const int m = threadIdx.x / TPR, sub = threadIdx.x % TPR;
     const int c0 = kb0 * BK, ncols = (kb1 - kb0) * BK;
-    for (int m = warp; m < MN; m += THREADS / 32) {
-      float mean = 0.f, rstd = 0.f;
-      const float* xr = nullptr;
-      if (m < M) {
-        const int2 ri = ln.rinfo[m];
-        xr = ln.x + ri.x * ln.x_sb + ri.y * ln.x_ss;
-        float s = 0.f, ss = 0.f;
-        for (int c = lane * 4; c < h; c += 128) {
-          const float4 v = *reinterpret_cast<const float4*>(xr + c);
-          s += v.x + v.y + v.z + v.w;
-          ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-        }
-        s = warp_sum(s);
-        ss = warp_sum(ss);
-        mean = s / (float)h;
-        rstd = 1.0f / sqrtf(fmaxf(ss / (float)h - mean * mean, 0.f) + 1e-5f);
+    const float* xr = ln.x;
+    float s = 0.f, ss = 0.f;
+    if (m < M) {
+      const int2 ri = ln.rinfo[m];
+      xr = ln.x + ri.x * ln.x_sb + ri.y * ln.x_ss;
+#pragma unroll 8
+      for (int c = sub * 4; c < h; c += TPR * 4) {
+        const float4 v = *reinterpret_cast<const float4*>(xr + c);
+        s += (v.x + v.y) + (v.z + v.w);
+        ss += (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
       }
-      // 8-column groups of this CTA's K range -> 16 B swizzled chunks
-      for (int grp = lane; grp < ncols / 8; grp += 32) {
-        const int col = c0 + grp * 8;
-        float y[8];
-        if (m < M && col < h) {
-          const float4 a = *reinterpret_cast<const float4*>(xr + col);
-          const float4 b = *reinterpret_cast<const float4*>(xr + col + 4);
-          const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    }
 #pragma unroll
-          for (int i = 0; i < 8; ++i) y[i] = (xv[i] - mean) * rstd * ln.g[col + i] + ln.b[col + i];
-        } else {
+    for (int o = 1; o < TPR; o <<= 1) {           // all lanes take part
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    const float mean = s / (float)h;
+    const float rstd = 1.0f / sqrtf(fmaxf(ss / (float)h - mean * mean, 0.f) + 1e-5f);
+    // 8-column groups of this CTA's K range -> 16 B swizzled chunks
+    for (int grp = sub; grp < ncols / 8; grp += TPR) {
+      const int col = c0 + grp * 8;
+      float y[8];
+      if (m < M && col < h) {
+        const float4 a = *reinterpret_cast<const float4*>(xr + col);
+        const float4 b = *reinterpret_cast<const float4*>(xr + col + 4);
+        const float4 g0 = *reinterpret_cast<const float4*>(ln.g + col);
+        const float4 g1 = *reinterpret_cast<const float4*>(ln.g + col + 4);
+        const float4 b0 = *reinterpret_cast<const float4*>(ln.b + col);
+        const float4 b1 = *reinterpret_cast<const float4*>(ln.b + col + 4);
+        const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-          for (int i = 0; i < 8; ++i) y[i] = 0.f;
-        }
-        const int tile = grp >> 3, chunk = grp & 7;
-        uint8_t* dst = sX + tile * L::X_TILE + (m >> 3) * 1024 + (m & 7) * 128 + ((chunk ^ (m & 7)) << 4);
-        store16<T>(reinterpret_cast<T*>(dst), y);
+        for (int i = 0; i < 8; ++i) y[i] = (xv[i] - mean) * rstd * gv[i] + bv[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = 0.f;
       }
+      const int tile = grp >> 3, chunk = grp & 7;
+      uint8_t* dst = sX + tile * L::X_TILE + (m >> 3) * 1024 + (m & 7) * 128 + ((chunk ^ (m & 7)) << 4);
+      store16<T>(reinterpret_cast<T*>(dst), y);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA
     mbar_arrive(x_ready);
@@ -292,7 +303,8 @@ bool gemv_tc_ln_sm100(int dtype, const float* x, long long x_sb, long long x_ss,
                       int M, int N, int K, const Epi& e, cudaStream_t st) {
   if (dtype == EET_F32 || M <= 0 || M > 32 || K % 64 != 0 || ldb % 8 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || (x_sb & 3) || (x_ss & 3) ||
-      (reinterpret_cast<uintptr_t>(B) & 15) || (K / 64 + gv::MAX_KBPS - 1) / gv::MAX_KBPS > 8)
+      (reinterpret_cast<uintptr_t>(B) & 15) || (K / 64 + gv::MAX_KBPS - 1) / gv::MAX_KBPS > 8 ||
+      (reinterpret_cast<uintptr_t>(g) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
     return false;
   const gv::LnSrc ln{x, x_sb, x_ss, rinfo, g, b};
   if (dtype == EET_BF16) {

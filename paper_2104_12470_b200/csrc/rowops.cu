@@ -345,6 +345,29 @@ void launch_argmax(const float* logits, int batch, int vocab, int* cur, long lon
   EET_LAUNCH_CHECK();
 }
 
+// x[valid row m] += reduced[m] : the residual add after a tensor-parallel
+// all-reduce (runtime.py:259 / :212 across shards).
+__global__ void residual_add_kernel(float* __restrict__ x, long long x_sb, long long x_ss,
+                                    const int2* __restrict__ rinfo, const float* __restrict__ r,
+                                    int h) {
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
+  const int m = blockIdx.x;
+  const int2 ri = rinfo[m];
+  float* xr = x + ri.x * x_sb + ri.y * x_ss;
+  const float* rr = r + (long long)m * h;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) xr[c] += rr[c];
+}
+
+void launch_residual_add(float* x, long long x_sb, long long x_ss, const int2* rinfo,
+                         const float* reduced, int rows, int h, cudaStream_t st) {
+  if (rows <= 0) return;
+  ProfScope ps(K_LAYERNORM, st, 12.0 * rows * h, 1.0 * rows * h);
+  launch_ex(residual_add_kernel, dim3(rows), dim3(256), 0, st, true, dim3(1, 1, 1), x, x_sb, x_ss,
+            rinfo, reduced, h);
+  EET_LAUNCH_CHECK();
+}
+
 __global__ void advance_kernel(int* d_filled, int* d_step) {
   sm100::griddep_wait();
   sm100::griddep_launch_dependents();

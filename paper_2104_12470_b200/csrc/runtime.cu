@@ -420,6 +420,8 @@ struct StepPlan {
 
 struct eet_runtime {
   int dtype, h, heads, hd, bmax, smax, splits;
+  int hq, ffn;                        // local Q/K/V width and FFN width (tensor-parallel shard)
+  int tp_rank = 0, tp_size = 1;
   eet_pool* pool;
   cudaStream_t cs = nullptr;          // private stream for graph capture
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
@@ -487,21 +489,23 @@ static void plan_fill(StepPlan& p, int batch, int t, const int* pads, int seq, i
   p.valid = true;
 }
 
-// One pre-norm layer over a prepared plan (runtime.py:217-263):
+// Attention half of a pre-norm layer over a prepared plan (runtime.py:106-189):
 //   LN1 (gather valid rows) -> QKV GEMM (epilogue: Q packed, K/V -> cache)
-//   -> mask-fused attention -> out-proj GEMM (epilogue: x += .)
-//   -> LN2 -> W1 GEMM (epilogue: GELU) -> W2 GEMM (epilogue: x += .)
-// Cache slot of local position 0 = (kv_dev ? *kv_dev : 0) + kv_base; the
-// device form lets a captured decode step advance without re-capture.
-static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb,
-                       long long x_ss, const eet_layer_weights* w, void* kc, void* vc,
-                       const int* kv_dev, int kv_base, bool causal, int L_host, cudaStream_t st) {
-  const int h = rt->h, T = p.T, dt = rt->dtype;
+//   -> mask-fused attention -> out-proj GEMM.
+// The out-proj epilogue adds into x (single GPU) or, for a tensor-parallel
+// shard, stores this rank's partial sum into `partial` ([T, h] fp32) for the
+// all-reduce. Cache slot of local position 0 = (kv_dev ? *kv_dev : 0) +
+// kv_base; the device form lets a captured decode step advance without
+// re-capture.
+static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb, long long x_ss,
+                       const eet_layer_weights* w, void* kc, void* vc, const int* kv_dev,
+                       int kv_base, bool causal, int L_host, float* partial, cudaStream_t st) {
+  const int h = rt->h, hq = rt->hq, T = p.T, dt = rt->dtype;
   const size_t es = dtype_size(dt);
   const int scope = (p.phase == EET_PHASE_PROMPT) ? EET_SCOPE_WITHIN : EET_SCOPE_ACROSS;
   if (T == 0) return;
 
-  Claim q(rt->pool, (size_t)T * h * es, scope, "attention.query");
+  Claim q(rt->pool, (size_t)T * hq * es, scope, "attention.query");
   {
     Epi e;
     e.mode = EPI_QKV;
@@ -512,30 +516,30 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
     e.vc = vc;
     e.heads = rt->heads;
     e.hd = rt->hd;
-    e.hq = h;
+    e.hq = hq;
     e.smax = rt->smax;
     e.kv_start = kv_dev;
     e.kv_base = kv_base;
     // decode rows: LN1 runs inside the GEMV prologue; otherwise LN -> GEMM
     if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b, w->wqkv, h,
-                                      T, 3 * h, h, e, st))) {
+                                      T, 3 * hq, h, e, st))) {
       Claim ln(rt->pool, (size_t)T * h * es, scope, "attention.layernorm");
       launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln1_g, w->ln1_b, ln.ptr, dt, h, h, 0, st);
-      gemm(dt, ln.ptr, h, w->wqkv, h, T, 3 * h, h, e, st);
+      gemm(dt, ln.ptr, h, w->wqkv, h, T, 3 * hq, h, e, st);
     }
   }
 
-  Claim ctx(rt->pool, (size_t)T * h * es, scope, "attention.context");
+  Claim ctx(rt->pool, (size_t)T * hq * es, scope, "attention.context");
   const float scale = 1.0f / std::sqrt((float)rt->hd);
   if (p.phase == EET_PHASE_PROMPT) {
     PrefillArgs a{};
     a.dtype = dt;
-    a.q = q.ptr; a.ldq = h; a.q_rowbase = p.rowbase;
+    a.q = q.ptr; a.ldq = hq; a.q_rowbase = p.rowbase;
     a.k = kc; a.v = vc;
     a.k_sb = (long long)rt->heads * rt->smax * rt->hd;
     a.k_sh = (long long)rt->smax * rt->hd;
     a.k_ss = rt->hd;
-    a.o = ctx.ptr; a.ldo = h; a.o_rowbase = p.rowbase;
+    a.o = ctx.ptr; a.ldo = hq; a.o_rowbase = p.rowbase;
     a.pads = p.pads;
     a.h_pads = p.h_pads.data();
     a.batch = p.batch; a.seq = p.seq; a.heads = rt->heads; a.hd = rt->hd;
@@ -547,7 +551,7 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
   } else {
     DecodeArgs a{};
     a.dtype = dt;
-    a.q = q.ptr; a.ldq = h;
+    a.q = q.ptr; a.ldq = hq;
     a.kc = kc; a.vc = vc;
     a.batch = p.batch; a.heads = rt->heads; a.hd = rt->hd; a.smax = rt->smax;
     a.pads = p.pads;
@@ -558,65 +562,102 @@ static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x
     a.scale = scale;
     a.part = rt->part;
     a.counters = rt->counters;
-    a.o = ctx.ptr; a.ldo = h;
+    a.o = ctx.ptr; a.ldo = hq;
     a.splits = rt->splits;
     launch_attn_decode(a, st);
   }
   q.release();
   {
     Epi e;
-    e.mode = EPI_RESID;
     e.bias = w->b_o;
-    e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
-    e.rinfo = p.rinfo;
-    gemm(dt, ctx.ptr, h, w->wo, h, T, h, h, e, st);
+    if (partial) {
+      e.mode = EPI_STORE_F32;
+      e.out = partial;
+      e.ldo = h;
+    } else {
+      e.mode = EPI_RESID;
+      e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
+      e.rinfo = p.rinfo;
+    }
+    gemm(dt, ctx.ptr, hq, w->wo, hq, T, h, hq, e, st);
   }
   ctx.release();
+}
 
-  // feed-forward block: both requests use across-module scope (runtime.py:200-207)
-  Claim mid(rt->pool, (size_t)T * 4 * h * es, EET_SCOPE_ACROSS, "ffn.intermediate");
+// Feed-forward half (runtime.py:192-214): LN2 -> W1 GEMM (+GELU) -> W2 GEMM,
+// residual into x or a tensor-parallel partial as above. Both pool requests
+// use across-module scope like the reference (runtime.py:200-207).
+static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb, long long x_ss,
+                      const eet_layer_weights* w, float* partial, cudaStream_t st) {
+  const int h = rt->h, f = rt->ffn, T = p.T, dt = rt->dtype;
+  const size_t es = dtype_size(dt);
+  if (T == 0) return;
+  Claim mid(rt->pool, (size_t)T * f * es, EET_SCOPE_ACROSS, "ffn.intermediate");
   {
     Epi e;
     e.mode = EPI_GELU_T;
     e.bias = w->b_1;
     e.out = mid.ptr;
-    e.ldo = 4 * h;
+    e.ldo = f;
     if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T,
-                                      4 * h, h, e, st))) {
+                                      f, h, e, st))) {
       Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
       launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln2_g, w->ln2_b, ln2.ptr, dt, h, h, 0, st);
-      gemm(dt, ln2.ptr, h, w->w1, h, T, 4 * h, h, e, st);
+      gemm(dt, ln2.ptr, h, w->w1, h, T, f, h, e, st);
     }
   }
   {
     Epi e;
-    e.mode = EPI_RESID;
     e.bias = w->b_2;
-    e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
-    e.rinfo = p.rinfo;
-    gemm(dt, mid.ptr, 4 * h, w->w2, 4 * h, T, h, 4 * h, e, st);
+    if (partial) {
+      e.mode = EPI_STORE_F32;
+      e.out = partial;
+      e.ldo = h;
+    } else {
+      e.mode = EPI_RESID;
+      e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
+      e.rinfo = p.rinfo;
+    }
+    gemm(dt, mid.ptr, f, w->w2, f, T, h, f, e, st);
   }
   mid.release();
 }
 
+// One whole pre-norm layer (runtime.py:217-263) on a single GPU.
+static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb,
+                       long long x_ss, const eet_layer_weights* w, void* kc, void* vc,
+                       const int* kv_dev, int kv_base, bool causal, int L_host, cudaStream_t st) {
+  attn_block(rt, p, x, x_sb, x_ss, w, kc, vc, kv_dev, kv_base, causal, L_host, nullptr, st);
+  ffn_block(rt, p, x, x_sb, x_ss, w, nullptr, st);
+}
+
 extern "C" {
 
-int eet_runtime_create(eet_runtime** out, int dtype, int hidden, int heads, int max_batch,
-                       int max_sequence, eet_pool* pool) {
-  EET_API_BEGIN
+// heads: heads held by this runtime (all of them, or one tensor-parallel
+// shard's); hd = hidden / heads_total.
+static eet_runtime* runtime_new(int dtype, int hidden, int heads_total, int tp_rank, int tp_size,
+                                int max_batch, int max_sequence, eet_pool* pool) {
   EET_REQUIRE(dtype == EET_F32 || dtype == EET_BF16 || dtype == EET_F16, EET_ERR_ARG, "bad dtype");
-  EET_REQUIRE(heads >= 1 && hidden % heads == 0, EET_ERR_ARG, "hidden not divisible by heads");
+  EET_REQUIRE(heads_total >= 1 && hidden % heads_total == 0, EET_ERR_ARG, "hidden not divisible by heads");
+  EET_REQUIRE(tp_size >= 1 && tp_rank >= 0 && tp_rank < tp_size, EET_ERR_ARG, "bad tensor-parallel rank");
+  EET_REQUIRE(heads_total % tp_size == 0 && (4 * hidden) % tp_size == 0, EET_ERR_ARG,
+              "heads and 4*hidden must divide by the tensor-parallel size");
   EET_REQUIRE(max_batch >= 1 && max_sequence >= 1, EET_ERR_ARG, "bad capacities");
   EET_REQUIRE(pool != nullptr && pool->device, EET_ERR_ARG, "runtime needs a device-backed buffer pool");
   std::unique_ptr<eet_runtime> rt(new eet_runtime());
+  const int heads = heads_total / tp_size;
   rt->dtype = dtype;
   rt->h = hidden;
   rt->heads = heads;
-  rt->hd = hidden / heads;
+  rt->hd = hidden / heads_total;
+  rt->hq = heads * rt->hd;
+  rt->ffn = 4 * hidden / tp_size;
+  rt->tp_rank = tp_rank;
+  rt->tp_size = tp_size;
   rt->bmax = max_batch;
   rt->smax = max_sequence;
   rt->pool = pool;
-  rt->splits = decode_splits(max_batch, heads, max_sequence, hidden / heads, (int)dtype_size(dtype));
+  rt->splits = decode_splits(max_batch, heads, max_sequence, rt->hd, (int)dtype_size(dtype));
   for (auto& p : rt->plans) plan_alloc(rt.get(), p);
   rt->part = (float*)rt->dev(sizeof(float) * (size_t)max_batch * heads * rt->splits * (rt->hd + 2));
   rt->counters = (int*)rt->dev(sizeof(int) * (size_t)max_batch * heads);
@@ -631,7 +672,20 @@ int eet_runtime_create(eet_runtime** out, int dtype, int hidden, int heads, int 
   EET_CHECK_CUDA(cudaEventCreateWithFlags(&rt->ev_in, cudaEventDisableTiming));
   EET_CHECK_CUDA(cudaEventCreateWithFlags(&rt->ev_out, cudaEventDisableTiming));
   EET_CHECK_CUDA(cudaDeviceSynchronize());
-  *out = rt.release();
+  return rt.release();
+}
+
+int eet_runtime_create(eet_runtime** out, int dtype, int hidden, int heads, int max_batch,
+                       int max_sequence, eet_pool* pool) {
+  EET_API_BEGIN
+  *out = runtime_new(dtype, hidden, heads, 0, 1, max_batch, max_sequence, pool);
+  EET_API_END
+}
+
+int eet_runtime_create_tp(eet_runtime** out, int dtype, int hidden, int heads_total, int tp_rank,
+                          int tp_size, int max_batch, int max_sequence, eet_pool* pool) {
+  EET_API_BEGIN
+  *out = runtime_new(dtype, hidden, heads_total, tp_rank, tp_size, max_batch, max_sequence, pool);
   EET_API_END
 }
 
@@ -678,6 +732,53 @@ int eet_encoder_layer_forward(eet_runtime* rt, float* x, long long x_sb, long lo
   Claim kbuf(rt->pool, kvb, EET_SCOPE_WITHIN, "attention.key");
   Claim vbuf(rt->pool, kvb, EET_SCOPE_WITHIN, "attention.value");
   layer_impl(rt, p, x, x_sb, x_ss, w, kbuf.ptr, vbuf.ptr, nullptr, 0, false, t, S(stream));
+  EET_API_END
+}
+
+// ------------------------------------------------------- tensor parallel
+static void check_layer_args(eet_runtime* rt, int batch, int t, int kv_filled, const int* h_pads,
+                             int seq_len, int phase) {
+  EET_REQUIRE(batch >= 1 && batch <= rt->bmax, EET_ERR_SHAPE, "batch exceeds runtime capacity");
+  if (phase == EET_PHASE_INCREMENTAL) {
+    EET_REQUIRE(t == 1, EET_ERR_SHAPE, "incremental step takes 1 token");
+    EET_REQUIRE(kv_filled >= seq_len, EET_ERR_SHAPE, "incremental phase before the prompt was cached");
+  } else {
+    EET_REQUIRE(t == seq_len, EET_ERR_SHAPE, "prompt pass length does not match seq_len");
+    EET_REQUIRE(kv_filled == 0, EET_ERR_SHAPE, "prompt phase expects an empty cache");
+  }
+  EET_REQUIRE(kv_filled + t <= rt->smax, EET_ERR_OVERFLOW, "step would overflow the cache");
+  for (int b = 0; b < batch; ++b)
+    EET_REQUIRE(h_pads[b] >= 0 && h_pads[b] < seq_len, EET_ERR_SHAPE, "pad outside [0, seq_len)");
+}
+
+int eet_tp_attention_partial(eet_runtime* rt, const float* x, long long x_sb, long long x_ss,
+                             int batch, int t, const eet_layer_weights* w, void* kc, void* vc,
+                             int kv_filled, const int* h_pads, int seq_len, int phase,
+                             float* partial, int* rows, void* stream) {
+  EET_API_BEGIN
+  check_layer_args(rt, batch, t, kv_filled, h_pads, seq_len, phase);
+  StepPlan& p = rt->plans[0];
+  plan_fill(p, batch, t, h_pads, seq_len, phase, S(stream));
+  if (rows) *rows = p.T;
+  attn_block(rt, p, const_cast<float*>(x), x_sb, x_ss, w, kc, vc, nullptr, kv_filled, true,
+             kv_filled + t, partial, S(stream));
+  EET_API_END
+}
+
+int eet_tp_ffn_partial(eet_runtime* rt, const float* x, long long x_sb, long long x_ss,
+                       const eet_layer_weights* w, float* partial, void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(rt->plans[0].valid, EET_ERR_ARG, "ffn partial before an attention partial");
+  ffn_block(rt, rt->plans[0], const_cast<float*>(x), x_sb, x_ss, w, partial, S(stream));
+  EET_API_END
+}
+
+int eet_tp_residual_add(eet_runtime* rt, float* x, long long x_sb, long long x_ss,
+                        const float* reduced, void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(rt->plans[0].valid, EET_ERR_ARG, "residual add before an attention partial");
+  const StepPlan& p = rt->plans[0];
+  launch_residual_add(x, x_sb, x_ss, p.rinfo, reduced, p.T, rt->h, S(stream));
   EET_API_END
 }
 

@@ -307,3 +307,50 @@ def test_generate_16bit_first_logits_vs_oracle(eet, dt):
     eet.generate(w, eet.GenerationRequest(prompts=prompts, steps=3), cfg, trace=tr)
     _, logs = orc.generate(orc.seeded_weights(256, 2, 4, 128, 32, 1), prompts, 3, 32, collect_logits=True)
     combined_close(tr.step_logits[0], logs[0], 2e-2, f"{dt} first logits")
+
+
+# --------------------------------------------------------- tensor parallel
+@pytest.mark.parametrize("dt,h,heads,tp,lengths", [("fp32", 256, 8, 2, [40, 17]),
+                                                   ("bf16", 1024, 8, 2, [300, 129]),
+                                                   ("bf16", 1536, 12, 4, [256])])
+def test_tensor_parallel_shards_sum_to_full_layer(eet, dt, h, heads, tp, lengths):
+    """tp ranks emulated on one GPU: every rank's attention / FFN partial
+    through the C ABI, summed (the all-reduce), residual-added — prompt pass
+    and one decode step — equal the unsharded oracle layer."""
+    from oracle import eet_oracle as orc
+    from paper_2104_12470_b200 import _lib
+    from paper_2104_12470_b200.tp import TensorParallelLayer, shard_config
+    desc = eet.make_batch(lengths)
+    s, b = desc.seq_len, len(lengths)
+    cfg = _cfg(eet, b, h, heads, s, s + 1, dt=dt)
+    w = eet.random_weights(cfg, vocab=8, seed=21).layers[0]
+    xh = np.random.default_rng(4).normal(0, 1, size=(b, s + 1, h)).astype(np.float32)
+    pool = eet.BufferPool()
+    ranks = [TensorParallelLayer(w, cfg, r, tp, pool) for r in range(tp)]
+    caches = [eet.preallocate_caches(shard_config(cfg, tp))[0] for _ in range(tp)]
+    x = torch.from_numpy(xh[:, :s].copy()).cuda()
+
+    def layer(x, phase):
+        parts = [rk.attention_partial(x, kv, desc, phase, 0) for rk, kv in zip(ranks, caches)]
+        total = torch.stack(parts).sum(0)
+        ranks[0].residual_add(x, total)
+        for rk in ranks:
+            rk._rows = total.shape[0]
+        ff = torch.stack([rk.ffn_partial(x) for rk in ranks]).sum(0)
+        ranks[0].residual_add(x, ff)
+
+    layer(x, _lib.PHASE_PROMPT)
+    for kv in caches:
+        kv.advance(s)
+    x1 = torch.from_numpy(xh[:, s:].copy()).cuda()
+    layer(x1, _lib.PHASE_INCREMENTAL)
+    om = orc.seeded_weights(h, 1, heads, 8, s + 1, 21)
+    okv = orc.OracleKV(b, heads, s + 1, h // heads, 1)
+    ref = orc.decoder_layer(xh[:, :s], om.layers[0], okv, desc.padding_len, 0, heads)
+    okv.advance(s)
+    ref1 = orc.decoder_layer(xh[:, s:], om.layers[0], okv, desc.padding_len, 0, heads)
+    tol = 1e-5 if dt == "fp32" else 2e-2
+    got = x.cpu().numpy()
+    for i, pad in enumerate(desc.padding_len):
+        combined_close(got[i, pad:], ref[i, pad:], tol, f"tp{tp} prompt row {i}")
+    combined_close(x1.cpu().numpy(), ref1, tol, f"tp{tp} decode step")
