@@ -33,6 +33,8 @@ namespace gv {
 using namespace sm100;
 
 constexpr int ROWS = 128, BK = 64, THREADS = 128, STAGES = 4, MAX_KBPS = 16;
+// LNX: a CTA's K-slice (<= LNX_MAX_COLS columns) of the token rows stays in registers
+constexpr int LNX_MAX_COLS = 256;
 constexpr int W_BYTES = ROWS * BK * 2;
 
 struct LnSrc {                      // LNX operand source
@@ -45,10 +47,11 @@ struct LnSrc {                      // LNX operand source
 
 template <int MN, bool LNX> struct Lay {
   static constexpr int X_TILE = MN * BK * 2;                 // one [MN x 64] operand tile
-  static constexpr int X_TILES = LNX ? MAX_KBPS : STAGES;    // whole K-range vs TMA ring
+  static constexpr int X_TILES = LNX ? LNX_MAX_COLS / BK : STAGES;   // whole K-slice vs TMA ring
   static constexpr int X_OFF = STAGES * W_BYTES;
   static constexpr int RED_OFF = X_OFF + X_TILES * X_TILE;
-  static constexpr int BAR_OFF = RED_OFF + ROWS * MN * 4;
+  static constexpr int STATS_OFF = RED_OFF + ROWS * MN * 4;   // LNX row stats [MN] float2
+  static constexpr int BAR_OFF = STATS_OFF + MN * 8;
   static constexpr int SMEM = BAR_OFF + 128 + 1024;
 };
 
@@ -63,6 +66,7 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   uint8_t* sW = smem;                                   // STAGES x 16 KB (1024-aligned)
   uint8_t* sX = smem + L::X_OFF;                        // X tiles (2-4 KB each, 1024-aligned)
   float* red = reinterpret_cast<float*>(smem + L::RED_OFF);        // [MN][128] partial tile
+  float2* stats = reinterpret_cast<float2*>(smem + L::STATS_OFF);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
@@ -108,50 +112,72 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
 
   if constexpr (LNX) {
     // ---- fused LayerNorm of the token rows into the swizzled X tiles.
-    // TPR threads per row, all rows at once: one pass of independent float4
-    // loads for the statistics, one for this CTA's columns.
-    constexpr int TPR = THREADS / MN;                   // 8 (MN 16) or 4 (MN 32)
+    // Every CTA of the split-K cluster loads only its own K-slice of the M
+    // rows (the columns it normalises), keeps it in registers, and the row
+    // statistics (sum, sum of squares) are combined across the cluster
+    // through DSMEM in rank order: one L2 round trip per CTA.
+    constexpr int TPR = THREADS / MN;                   // threads per row: 8 (MN 16) / 4 (MN 32)
+    constexpr int GPT = LNX_MAX_COLS / 8 / TPR;         // 8-column groups per thread
     const int h = K;
     const int m = threadIdx.x / TPR, sub = threadIdx.x % TPR;
-    const int c0 = kb0 * BK, ncols = (kb1 - kb0) * BK;
+    const int c0 = kb0 * BK, ngrp = (kb1 - kb0) * BK / 8;
     const float* xr = ln.x;
-    float s = 0.f, ss = 0.f;
     if (m < M) {
       const int2 ri = ln.rinfo[m];
       xr = ln.x + ri.x * ln.x_sb + ri.y * ln.x_ss;
-#pragma unroll 8
-      for (int c = sub * 4; c < h; c += TPR * 4) {
-        const float4 v = *reinterpret_cast<const float4*>(xr + c);
-        s += (v.x + v.y) + (v.z + v.w);
-        ss += (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
+    }
+    float v[GPT][8];
+    float s = 0.f, ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < GPT; ++i) {                     // all loads in flight together
+      const int grp = sub + i * TPR;
+      if (m < M && grp < ngrp) {
+        const float4 a = *reinterpret_cast<const float4*>(xr + c0 + grp * 8);
+        const float4 b = *reinterpret_cast<const float4*>(xr + c0 + grp * 8 + 4);
+        v[i][0] = a.x; v[i][1] = a.y; v[i][2] = a.z; v[i][3] = a.w;
+        v[i][4] = b.x; v[i][5] = b.y; v[i][6] = b.z; v[i][7] = b.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] = 0.f;
       }
     }
+#pragma unroll
+    for (int i = 0; i < GPT; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { s += v[i][j]; ss += v[i][j] * v[i][j]; }
 #pragma unroll
     for (int o = 1; o < TPR; o <<= 1) {           // all lanes take part
       s += __shfl_xor_sync(0xffffffffu, s, o);
       ss += __shfl_xor_sync(0xffffffffu, ss, o);
     }
-    const float mean = s / (float)h;
-    const float rstd = 1.0f / sqrtf(fmaxf(ss / (float)h - mean * mean, 0.f) + 1e-5f);
-    // 8-column groups of this CTA's K range -> 16 B swizzled chunks
-    for (int grp = sub; grp < ncols / 8; grp += TPR) {
+    if (sub == 0) stats[m] = make_float2(s, ss);
+    cluster_sync();
+    float ts = 0.f, tss = 0.f;
+    for (int p = 0; p < splits; ++p) {            // rank order: deterministic
+      const float2 q = map_peer(stats, p)[m];
+      ts += q.x;
+      tss += q.y;
+    }
+    const float mean = ts / (float)h;
+    const float rstd = 1.0f / sqrtf(fmaxf(tss / (float)h - mean * mean, 0.f) + 1e-5f);
+#pragma unroll
+    for (int i = 0; i < GPT; ++i) {
+      const int grp = sub + i * TPR;
+      if (grp >= ngrp) continue;
       const int col = c0 + grp * 8;
       float y[8];
-      if (m < M && col < h) {
-        const float4 a = *reinterpret_cast<const float4*>(xr + col);
-        const float4 b = *reinterpret_cast<const float4*>(xr + col + 4);
+      if (m < M) {
         const float4 g0 = *reinterpret_cast<const float4*>(ln.g + col);
         const float4 g1 = *reinterpret_cast<const float4*>(ln.g + col + 4);
         const float4 b0 = *reinterpret_cast<const float4*>(ln.b + col);
         const float4 b1 = *reinterpret_cast<const float4*>(ln.b + col + 4);
-        const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
         const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
         const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = (xv[i] - mean) * rstd * gv[i] + bv[i];
+        for (int j = 0; j < 8; ++j) y[j] = (v[i][j] - mean) * rstd * gv[j] + bv[j];
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = 0.f;
+        for (int j = 0; j < 8; ++j) y[j] = 0.f;
       }
       const int tile = grp >> 3, chunk = grp & 7;
       uint8_t* dst = sX + tile * L::X_TILE + (m >> 3) * 1024 + (m & 7) * 128 + ((chunk ^ (m & 7)) << 4);
@@ -250,7 +276,7 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
 static void plan_splits(int rbs, int nkb, bool lnx, int* splits, int* kbps) {
   const int target = 2 * device_sm_count();
   int s = std::min(std::max(1, (target + rbs - 1) / rbs), std::min(nkb, 8));
-  if (lnx) s = std::max(s, (nkb + MAX_KBPS - 1) / MAX_KBPS);
+  if (lnx) s = std::max(s, (nkb * BK + LNX_MAX_COLS - 1) / LNX_MAX_COLS);
   const int k = (nkb + s - 1) / s;
   *kbps = k;
   *splits = (nkb + k - 1) / k;
@@ -303,7 +329,7 @@ bool gemv_tc_ln_sm100(int dtype, const float* x, long long x_sb, long long x_ss,
                       int M, int N, int K, const Epi& e, cudaStream_t st) {
   if (dtype == EET_F32 || M <= 0 || M > 32 || K % 64 != 0 || ldb % 8 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || (x_sb & 3) || (x_ss & 3) ||
-      (reinterpret_cast<uintptr_t>(B) & 15) || (K / 64 + gv::MAX_KBPS - 1) / gv::MAX_KBPS > 8 ||
+      (reinterpret_cast<uintptr_t>(B) & 15) || (K + gv::LNX_MAX_COLS - 1) / gv::LNX_MAX_COLS > 8 ||
       (reinterpret_cast<uintptr_t>(g) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
     return false;
   const gv::LnSrc ln{x, x_sb, x_ss, rinfo, g, b};
