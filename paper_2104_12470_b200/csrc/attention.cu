@@ -377,32 +377,34 @@ __global__ void __launch_bounds__(DWARPS * 32) attn_decode_kernel(DecodeArgs a) 
   if (threadIdx.x == 0) a.counters[b * a.heads + head] = 0;
 }
 
-// Streaming variant: the split's K and V rows are contiguous in the
-// [b, heads, s_max, hd] cache, so a producer warp moves them into a
-// two-chunk shared-memory ring with TMA bulk copies (64 keys per chunk,
-// full/empty mbarriers) while the four compute warps consume the other
-// chunk. 32 KB of ring per CTA (hd 64, 16-bit) keeps ~7 CTAs per SM, one
-// wave for the c2 decode step. Requires 16-byte key rows.
+// Streaming variant: the K and V rows of a (sequence, head) are contiguous in
+// the [b, heads, s_max, hd] cache, so a producer warp moves them into a
+// shared-memory ring with TMA bulk copies (64 keys per chunk, full/empty
+// mbarriers) while 8 compute warps consume earlier chunks. With enough
+// (sequence, head) pairs to fill the GPU (c2: 16 x 16) each CTA owns a whole
+// pair and there is nothing to combine; small batches split the key range
+// and the last CTA of a pair merges the splits. Requires 16-byte key rows.
 constexpr int DCHUNK = 64;
+constexpr int CWARPS = 8;
 
-template <typename T, int E, int LPK>
-__global__ void __launch_bounds__((DWARPS + 1) * 32) attn_decode_bulk_kernel(DecodeArgs a) {
+template <typename T, int E, int LPK, int NBUF>
+__global__ void __launch_bounds__((CWARPS + 1) * 32) attn_decode_bulk_kernel(DecodeArgs a) {
   constexpr int G = 32 / LPK;
   extern __shared__ __align__(128) uint8_t dsm[];
-  __shared__ __align__(8) uint64_t full[2], empty[2];
-  __shared__ float sm_m[DWARPS], sm_l[DWARPS];
-  __shared__ float sm_acc[DWARPS][LPK * E];
+  __shared__ __align__(8) uint64_t full[NBUF], empty[NBUF];
+  __shared__ float sm_m[CWARPS], sm_l[CWARPS];
+  __shared__ float sm_acc[CWARPS][LPK * E];
   __shared__ int sm_last;
   const int split = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / LPK, sub = lane % LPK;
   const int hd = a.hd;
   const size_t chunk_elems = (size_t)DCHUNK * hd;
-  T* ring = reinterpret_cast<T*>(dsm);                    // [2][K chunk | V chunk]
+  T* ring = reinterpret_cast<T*>(dsm);                    // [NBUF][K chunk | V chunk]
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], DWARPS);
+      sm100::mbar_init(&empty[i], CWARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -418,13 +420,13 @@ __global__ void __launch_bounds__((DWARPS + 1) * 32) attn_decode_bulk_kernel(Dec
   const int nch = (nk + DCHUNK - 1) / DCHUNK;
   const long long base = ((long long)b * a.heads + head) * a.smax * hd;
 
-  if (warp == DWARPS) {                   // ---- producer warp
+  if (warp == CWARPS) {                   // ---- producer warp
     if (lane == 0) {
       const T* Kc = reinterpret_cast<const T*>(a.kc) + base + (long long)ks * hd;
       const T* Vc = reinterpret_cast<const T*>(a.vc) + base + (long long)ks * hd;
       for (int c = 0; c < nch; ++c) {
-        const int buf = c & 1;
-        if (c >= 2) sm100::mbar_wait(&empty[buf], ((c >> 1) - 1) & 1);
+        const int buf = c % NBUF;
+        if (c >= NBUF) sm100::mbar_wait(&empty[buf], ((c / NBUF) - 1) & 1);
         const int kn = min(DCHUNK, nk - c * DCHUNK);
         const uint32_t bytes = (uint32_t)(kn * hd * sizeof(T));
         T* dst = ring + buf * 2 * chunk_elems;
@@ -448,12 +450,12 @@ __global__ void __launch_bounds__((DWARPS + 1) * 32) attn_decode_bulk_kernel(Dec
 #pragma unroll
     for (int e = 0; e < E; ++e) acc[e] = 0.f;
     for (int c = 0; c < nch; ++c) {
-      const int buf = c & 1;
-      sm100::mbar_wait(&full[buf], (c >> 1) & 1);
+      const int buf = c % NBUF;
+      sm100::mbar_wait(&full[buf], (c / NBUF) & 1);
       const T* sK = ring + buf * 2 * chunk_elems;
       const T* sV = sK + chunk_elems;
       const int kn = min(DCHUNK, nk - c * DCHUNK);
-      for (int jb = warp * G; jb < kn; jb += DWARPS * G) {     // warp-uniform
+      for (int jb = warp * G; jb < kn; jb += CWARPS * G) {     // warp-uniform
         const int j = jb + g;
         const bool ok = j < kn;
         float kv[E], vv[E];
@@ -512,29 +514,33 @@ __global__ void __launch_bounds__((DWARPS + 1) * 32) attn_decode_bulk_kernel(Dec
   if (warp == 0) {
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < DWARPS; ++w) M = fmaxf(M, sm_m[w]);
-    float Lsum = 0.f, cw[DWARPS];
+    for (int w = 0; w < CWARPS; ++w) M = fmaxf(M, sm_m[w]);
+    float Lsum = 0.f, cw[CWARPS];
 #pragma unroll
-    for (int w = 0; w < DWARPS; ++w) {
+    for (int w = 0; w < CWARPS; ++w) {
       cw[w] = (sm_m[w] == -INFINITY) ? 0.f : expf(sm_m[w] - M);
       Lsum += sm_l[w] * cw[w];
     }
     for (int d = lane; d < hd; d += 32) {
       float v = 0.f;
 #pragma unroll
-      for (int w = 0; w < DWARPS; ++w) v += sm_acc[w][d] * cw[w];
+      for (int w = 0; w < CWARPS; ++w) v += sm_acc[w][d] * cw[w];
       if (a.splits == 1) reinterpret_cast<T*>(a.o)[(long long)b * a.ldo + head * hd + d] = from_f<T>(v / Lsum);
       else part[d] = v;
     }
     if (lane == 0 && a.splits > 1) { part[hd] = M; part[hd + 1] = Lsum; }
   }
   if (a.splits == 1) return;
-  __threadfence();
+  // last split of the pair merges: barrier + one acq_rel atomic (release of
+  // this CTA's partial, acquire of everyone else's) instead of SC fences
   __syncthreads();
-  if (threadIdx.x == 0) sm_last = (atomicAdd(&a.counters[b * a.heads + head], 1) == a.splits - 1);
+  if (threadIdx.x == 0) {
+    int prev;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(&a.counters[b * a.heads + head]) : "memory");
+    sm_last = (prev == a.splits - 1);
+  }
   __syncthreads();
   if (!sm_last) return;
-  __threadfence();
   const float* p0 = a.part + ((long long)b * a.heads + head) * a.splits * (hd + 2);
   float M = -INFINITY;
   for (int s2 = 0; s2 < a.splits; ++s2) M = fmaxf(M, __ldcg(p0 + s2 * (hd + 2) + hd));
@@ -559,7 +565,7 @@ __global__ void __launch_bounds__((DWARPS + 1) * 32) attn_decode_bulk_kernel(Dec
 int decode_splits(int batch, int heads, int smax, int hd, int es) {
   (void)hd; (void)es;
   const int pairs = std::max(1, batch * heads);
-  const int by_len = (smax + 255) / 256;
+  const int by_len = 1;                                // streaming ring: no length limit
   const int by_sms = (2 * 148 + pairs - 1) / pairs;
   const int cap = std::max(1, (smax + 31) / 32);       // >= 32 keys per split
   return std::max(1, std::min(std::max(by_len, by_sms), std::min(cap, 64)));
@@ -583,6 +589,7 @@ static void decode_launch(const DecodeArgs& a, cudaStream_t st) {
 
 template <typename T, int E, int LPK>
 static void decode_bulk_launch(const DecodeArgs& a, cudaStream_t st) {
+  constexpr int NBUF = (E * LPK * sizeof(T) <= 128) ? 4 : 2;   // ring <= 64 KB
   dim3 grid(a.splits, a.heads, a.batch);
   double keys = 0;
   for (int b = 0; b < a.batch; ++b)
@@ -590,12 +597,12 @@ static void decode_bulk_launch(const DecodeArgs& a, cudaStream_t st) {
   const double es = (double)sizeof(T);
   const double per_key_b = (double)a.heads * a.hd * 2 * es, per_key_f = (double)a.heads * 4.0 * a.hd;
   if (a.L_host < 0) keys = 0;
-  const size_t smem = (size_t)2 * 2 * DCHUNK * a.hd * sizeof(T);
-  auto kern = attn_decode_bulk_kernel<T, E, LPK>;
+  const size_t smem = (size_t)NBUF * 2 * DCHUNK * a.hd * sizeof(T);
+  auto kern = attn_decode_bulk_kernel<T, E, LPK, NBUF>;
   EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ProfScope ps(K_ATTN_DECODE, st, keys * per_key_b + 2.0 * a.batch * a.heads * a.hd * es,
                keys * per_key_f, a.L_host >= 0 ? 0.0 : per_key_b, a.L_host >= 0 ? 0.0 : per_key_f);
-  launch_ex(kern, grid, dim3((DWARPS + 1) * 32), smem, st, true, dim3(1, 1, 1), a);
+  launch_ex(kern, grid, dim3((CWARPS + 1) * 32), smem, st, true, dim3(1, 1, 1), a);
   EET_LAUNCH_CHECK();
 }
 

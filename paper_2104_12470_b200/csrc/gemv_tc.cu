@@ -332,6 +332,11 @@ bool gemv_tc_ln_sm100(int dtype, const float* x, long long x_sb, long long x_ss,
       (reinterpret_cast<uintptr_t>(B) & 15) || (K + gv::LNX_MAX_COLS - 1) / gv::LNX_MAX_COLS > 8 ||
       (reinterpret_cast<uintptr_t>(g) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
     return false;
+  {
+    int sp, kb;
+    gv::plan_splits((N + gv::ROWS - 1) / gv::ROWS, K / 64, false, &sp, &kb);
+    if (kb * 64 > gv::LNX_MAX_COLS) return false;       // e.g. LM head: 1 split of 1024 columns
+  }
   const gv::LnSrc ln{x, x_sb, x_ss, rinfo, g, b};
   if (dtype == EET_BF16) {
     M <= 16 ? gv::launch<__nv_bfloat16, 16, true>(nullptr, 0, ln, B, ldb, M, N, K, e, dtype, st)
