@@ -2,41 +2,45 @@
 // head_dim 64 / 128 (§2.1 Algorithm 1; attention.py:73-104 +
 // runtime.py:164-178 in the reference).
 //
-// One CTA = one (sequence b, head, 128-query tile). Causal and padding
-// bounds come from slot indices: key tiles start at the sequence's pad
-// offset and stop at the tile's last query, so pad keys are never loaded and
-// query tiles that lie wholly in the padding exit immediately.
+// One CTA = one (sequence b, head, pair of 128-query tiles A/B). Causal and
+// padding bounds come from slot indices: key tiles start at the sequence's
+// pad offset and stop at each query tile's last query, so pad keys are never
+// loaded and query tiles that lie wholly in the padding exit immediately.
 //
-//   warp 0      TMA producer: Q tile once, then K/V tiles (128 keys) into a
-//               two-stage ring, straight from the [b, heads, s_max, hd] cache.
-//   warp 1      TMEM allocator + MMA issuer: S_j = Q K_j^T (M=128, N=128,
-//               K-major both) into one of two TMEM score buffers, then
-//               O_j = P_j V_j (M=128, N=hd; P K-major from smem, V MN-major).
-//   warps 2..5  softmax: thread = query row; reads its S row from TMEM,
-//               applies the index-derived mask, online max/sum in fp32,
-//               writes P (16-bit, 128B-swizzled) to smem, then folds O_j into
-//               a register accumulator with the running correction.
-// The score matrix never reaches HBM; S_{j+1} overlaps the softmax of S_j.
+//   warps 0-3   softmax for tile A, warps 4-7 for tile B (thread = query row)
+//   warp 8      TMA producer: Q_A, Q_B once, then K/V tiles (64 keys) into a
+//               two-stage ring straight from the [b, heads, s_max, hd] cache
+//   warp 9      TMEM allocator + MMA issuer: S_X = Q_X K_j^T (M128 N64) and
+//               O_X += P_X V_j (M128 N=hd; P K-major from smem, V MN-major)
+//
+// O accumulates in TMEM across key tiles; a softmax thread rescales its O
+// row (tcgen05.ld/st) only when its running max grows by more than 2^8
+// (lazy rescaling), so the common tile costs one TMEM read of S and one
+// smem write of P per row. With two query tiles the tensor core works on
+// one tile while the softmax warps of the other run.
 #include "sm100.cuh"
 
 namespace eet {
 namespace fa {
 using namespace sm100;
 
-constexpr int BQ = 128, BKV = 128, THREADS = 192;
+constexpr int BQ = 128, BKV = 64, NSM = 8, THREADS = (NSM + 2) * 32;
+constexpr float RESCALE_LOG2 = 8.0f;       // lazy rescale threshold (log2 units)
 
 template <int HD> struct Cfg {
   static constexpr int KSUB = HD / 64;                  // 64-wide (128 B) K-atoms per row
-  static constexpr int SUB = 128 * 128;                 // one 128-row x 128 B sub-tile
-  static constexpr int Q_BYTES = KSUB * SUB;
-  static constexpr int KV_BYTES = KSUB * SUB;           // K tile (V tile same size)
-  static constexpr int P_BYTES = 2 * SUB;               // 128 queries x 128 keys
-  static constexpr int SMEM = Q_BYTES + 4 * KV_BYTES + P_BYTES + 1024 + 256;
-  static constexpr uint32_t S_COL = 0, O_COL = 256;     // TMEM: S0 | S1 | O
+  static constexpr int QSUB = BQ * 128;                 // 128 rows x 128 B
+  static constexpr int KVSUB = BKV * 128;               //  64 rows x 128 B
+  static constexpr int Q_BYTES = KSUB * QSUB;           // one query tile
+  static constexpr int KV_BYTES = KSUB * KVSUB;         // one K (or V) tile
+  static constexpr int P_BYTES = BQ * BKV * 2;          // 128 queries x 64 keys, one atom wide
+  static constexpr int SMEM = 2 * Q_BYTES + 4 * KV_BYTES + 2 * P_BYTES + 1024 + 256;
+  // TMEM columns: S_A | S_B | O_A | O_B
+  static constexpr uint32_t S_COL = 0, O_COL = 2 * BKV;
 };
 
-// K-major SW128 descriptor is sm100::smem_desc; V is read MN-major:
-// 8-key row groups 1024 B apart (SBO), 64-wide hd blocks one sub-tile apart (LBO).
+// V is read MN-major: 8-key row groups 1024 B apart (SBO), 64-wide hd blocks
+// one sub-tile apart (LBO).
 __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t saddr, uint32_t lbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
@@ -45,10 +49,6 @@ __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t saddr, uint32_t lbo) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
-}
-
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf) {
@@ -60,13 +60,25 @@ __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 struct FaArgs {
   const int* pads;          // [b]
   const int* q_rowbase;     // packed row of slot s = q_rowbase[b] + s
   void* o; int ldo;
   int batch, seq, heads, smax, causal;
   float scale_log2;         // (1/sqrt(hd)) * log2(e)
-  float scale;              // 1/sqrt(hd)
 };
 
 template <typename T, int HD>
@@ -76,31 +88,33 @@ __global__ void __launch_bounds__(THREADS, 1)
   using C = Cfg<HD>;
   constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
   const int b = blockIdx.z, head = blockIdx.y;
-  const int n_qt = gridDim.x;
-  const int qt = n_qt - 1 - blockIdx.x;                  // heaviest (latest) tiles first
-  const int q0 = qt * BQ;
+  const int npair = gridDim.x;
+  const int pair = npair - 1 - blockIdx.x;                // heaviest (latest) queries first
+  const int q0 = pair * 2 * BQ;
   const int pad = a.pads[b];
-  const int qhi = min(q0 + BQ, a.seq);
-  if (qhi <= pad) return;                                 // tile wholly in the padding
-  const int kend = a.causal ? qhi : a.seq;                // keys [pad, kend)
-  const int nt = (kend - pad + BKV - 1) / BKV;
+  const int qhiA = min(q0 + BQ, a.seq), qhiB = min(q0 + 2 * BQ, a.seq);
+  if (qhiB <= pad) return;                                // both tiles in the padding
+  const bool liveA = qhiA > pad && q0 < a.seq;
+  const int kendA = a.causal ? qhiA : a.seq, kendB = a.causal ? qhiB : a.seq;
+  const int ntA = liveA ? (kendA - pad + BKV - 1) / BKV : 0;
+  const int ntB = (kendB - pad + BKV - 1) / BKV;          // B's range covers A's
+  const int nt = ntB;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sK = sQ + C::Q_BYTES;                          // [2] stages
+  uint8_t* sQ = sm;                                       // [2] query tiles
+  uint8_t* sK = sQ + 2 * C::Q_BYTES;                      // [2] stages
   uint8_t* sV = sK + 2 * C::KV_BYTES;                     // [2] stages
-  uint8_t* sP = sV + 2 * C::KV_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::P_BYTES);
+  uint8_t* sP = sV + 2 * C::KV_BYTES;                     // [2] tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;      // [2]
   uint64_t* kv_empty = bars + 3;     // [2]
-  uint64_t* s_full = bars + 5;       // [2]
-  uint64_t* p_full = bars + 7;
-  uint64_t* o_full = bars + 8;
-  uint64_t* o_empty = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* s_full = bars + 5;       // [2] per tile
+  uint64_t* p_full = bars + 7;       // [2]
+  uint64_t* o_done = bars + 9;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -109,164 +123,172 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_done[i], 1);
     }
-    mbar_init(p_full, 128);
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapQ) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapK) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapV) : "memory");
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == NSM + 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int kv_row0 = (b * a.heads + head) * a.smax;      // cache row of slot 0
 
-  if (warp == 0) {
+  if (warp == NSM) {
     if (lane == 0) {
-      const uint64_t pol = 0x14F0000000000000ull;         // EVICT_LAST: K/V reused by q tiles
-      mbar_expect_tx(q_full, C::Q_BYTES);
-      for (int s = 0; s < C::KSUB; ++s)
-        tma_load_2d(sQ + s * C::SUB, &mapQ, q_full, head * HD + 64 * s, a.q_rowbase[b] + q0, pol);
+      const uint64_t pol = 0x14F0000000000000ull;         // EVICT_LAST: K/V reused by query tiles
+      mbar_expect_tx(q_full, 2 * C::Q_BYTES);
+      for (int t = 0; t < 2; ++t)
+        for (int s = 0; s < C::KSUB; ++s)
+          tma_load_2d(sQ + t * C::Q_BYTES + s * C::QSUB, &mapQ, q_full, head * HD + 64 * s,
+                      a.q_rowbase[b] + q0 + t * BQ, pol);
       for (int j = 0; j < nt; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
         const int row = kv_row0 + pad + j * BKV;
         for (int s = 0; s < C::KSUB; ++s) {
-          tma_load_2d(sK + st * C::KV_BYTES + s * C::SUB, &mapK, &kv_full[st], 64 * s, row, pol);
-          tma_load_2d(sV + st * C::KV_BYTES + s * C::SUB, &mapV, &kv_full[st], 64 * s, row, pol);
+          tma_load_2d(sK + st * C::KV_BYTES + s * C::KVSUB, &mapK, &kv_full[st], 64 * s, row, pol);
+          tma_load_2d(sV + st * C::KV_BYTES + s * C::KVSUB, &mapV, &kv_full[st], 64 * s, row, pol);
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == NSM + 1) {
     if (lane == 0) {
       constexpr uint32_t fmt = BF ? 1 : 0;
       constexpr uint32_t id_s = instr_desc(fmt, BQ, BKV);
       constexpr uint32_t id_o = instr_desc(fmt, BQ, HD) | (1u << 16);   // B (V) MN-major
-      const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
-      auto issue_s = [&](int j) {
-        const int st = j & 1;
-        const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t off = (k >> 2) * C::SUB + (k & 3) * 32;
-          mma_f16(tmem + C::S_COL + st * 128, smem_desc(q_base + off), smem_desc(k_base + off), id_s,
-                  k > 0);
-        }
-        mma_commit(&s_full[st]);
-      };
       mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[0], 0);
-      tc_fence_after();
-      issue_s(0);
       for (int j = 0; j < nt; ++j) {
-        if (j + 1 < nt) {
-          mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-          tc_fence_after();
-          issue_s(j + 1);
-        }
-        mbar_wait(p_full, j & 1);
-        mbar_wait(o_empty, (j & 1) ^ 1);
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t v_base = smem_u32(sV + (j & 1) * C::KV_BYTES);
+        const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
+        const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
+        for (int t = 0; t < 2; ++t) {                     // S_t = Q_t K_j^T
+          if (t == 0 && j >= ntA) continue;
+          const uint32_t q_base = smem_u32(sQ + t * C::Q_BYTES);
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {
-          const uint32_t poff = (k >> 2) * C::SUB + (k & 3) * 32;
-          mma_f16(tmem + C::O_COL, smem_desc(p_base + poff), smem_desc_mn(v_base + k * 2048, C::SUB),
-                  id_o, k > 0);
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint32_t qoff = (k >> 2) * C::QSUB + (k & 3) * 32;
+            const uint32_t koff = (k >> 2) * C::KVSUB + (k & 3) * 32;
+            mma_f16(tmem + C::S_COL + t * BKV, smem_desc(q_base + qoff), smem_desc(k_base + koff),
+                    id_s, k > 0);
+          }
+          mma_commit(&s_full[t]);
         }
-        mma_commit(o_full);
-        mma_commit(&kv_empty[j & 1]);
+        for (int t = 0; t < 2; ++t) {                     // O_t += P_t V_j
+          if (t == 0 && j >= ntA) continue;
+          mbar_wait(&p_full[t], j & 1);
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(sP + t * C::P_BYTES);
+#pragma unroll
+          for (int k = 0; k < BKV / 16; ++k)
+            mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
+                    smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
+          mma_commit(&o_done[t]);
+        }
+        mma_commit(&kv_empty[st]);
       }
     }
   } else {
-    // ---- softmax warps: thread <-> query row
+    // ---- softmax warps: thread <-> query row of tile t
+    const int t = warp >> 2;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
-    const int qs = q0 + row;
+    const int qs = q0 + t * BQ + row;
+    const int ntile = t == 0 ? ntA : ntB;
     const bool live = qs >= pad && qs < a.seq;
     const int row_kend = live ? (a.causal ? qs + 1 : a.seq) : pad;   // keys [pad, row_kend)
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    float m = -INFINITY, l = 0.f;
-    float o[HD];
-#pragma unroll
-    for (int d = 0; d < HD; ++d) o[d] = 0.f;
-    uint8_t* prow = sP + row * 128;
-    for (int j = 0; j < nt; ++j) {
+    const uint32_t s_addr = tmem + lane_addr + C::S_COL + t * BKV;
+    const uint32_t o_addr = tmem + lane_addr + C::O_COL + t * HD;
+    uint8_t* prow = sP + t * C::P_BYTES + row * 128;
+    float m = -INFINITY, l = 0.f;                         // m in log2 units (scaled)
+    for (int j = 0; j < ntile; ++j) {
       const int kt = pad + j * BKV;
-      const int nvalid = min(max(row_kend - kt, 0), BKV);      // keys [kt, kt+nvalid) count
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      const int nvalid = min(max(row_kend - kt, 0), BKV);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const uint32_t s_addr = tmem + lane_addr + C::S_COL + (j & 1) * 128;
+      float sv[BKV];
+      {
+        uint32_t r[32];
+        tmem_ld32(s_addr, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[i] = __uint_as_float(r[i]);
+        tmem_ld32(s_addr + 32, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[32 + i] = __uint_as_float(r[i]);
+      }
       float tmax = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(s_addr + c * 32, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < nvalid) tmax = fmaxf(tmax, __uint_as_float(r[i]) * a.scale);
+      for (int i = 0; i < BKV; ++i) {
+        sv[i] = (i < nvalid) ? sv[i] * a.scale_log2 : -INFINITY;
+        tmax = fmaxf(tmax, sv[i]);
       }
-      const float m_new = fmaxf(m, tmax);
-      const float corr = (m == -INFINITY) ? (m_new == -INFINITY ? 1.f : 0.f)
-                                          : exp2f((m - m_new) * 1.4426950408889634f);
-      const float msub = (m_new == -INFINITY) ? 0.f : m_new * 1.4426950408889634f;
+      // O rows and P buffer of tile j-1 must be done before we touch them
+      if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);
+      tc_fence_after();
+      if (tmax > m + RESCALE_LOG2 || (m == -INFINITY && tmax != -INFINITY)) {
+        const float m_new = fmaxf(m, tmax);
+        if (m != -INFINITY) {                             // rescale O and l
+          const float f = exp2f(m - m_new);
+          l *= f;
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t r[32];
+            tmem_ld32(o_addr + c * 32, r);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+            tmem_st32(o_addr + c * 32, r);
+          }
+        }
+        m = m_new;
+      }
+      const float msub = (m == -INFINITY) ? 0.f : m;
       float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld32(s_addr + c * 32, r);
-        uint32_t pk[16];
+      for (int c = 0; c < BKV / 8; ++c) {                 // 8 keys -> one 16 B swizzled chunk
+        uint32_t pk[4];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float p0 = (c * 32 + i < nvalid) ? exp2f(__uint_as_float(r[i]) * a.scale_log2 - msub) : 0.f;
-          float p1 = (c * 32 + i + 1 < nvalid) ? exp2f(__uint_as_float(r[i + 1]) * a.scale_log2 - msub) : 0.f;
+        for (int i = 0; i < 8; i += 2) {
+          const float p0 = exp2f(sv[c * 8 + i] - msub);
+          const float p1 = exp2f(sv[c * 8 + i + 1] - msub);
           rs += p0 + p1;
           pk[i >> 1] = pack2(p0, p1, BF);
         }
-        // keys c*32 .. c*32+31 -> sub-tile c/2, 16B chunks (c%2)*4 .. +3, 128B-swizzled
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int chunk = (c & 1) * 4 + q;
-          uint8_t* dst = prow + (c >> 1) * C::SUB + ((chunk ^ (row & 7)) << 4);
-          *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
+        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      l = l * corr + rs;
-      m = m_new;
-      fence_async_smem();                    // P writes -> visible to the tensor core
+      l += rs;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
       tc_fence_before();
-      mbar_arrive(p_full);
-      mbar_wait(o_full, j & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_addr + C::O_COL + c * 32, r);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[c * 32 + i] = o[c * 32 + i] * corr + __uint_as_float(r[i]);
-      }
-      tc_fence_before();
-      mbar_arrive(o_empty);
+      mbar_arrive(&p_full[t]);
     }
-    if (live) {
+    if (ntile > 0) mbar_wait(&o_done[t], (ntile - 1) & 1);
+    tc_fence_after();
+    if (live && ntile > 0) {
       const float inv = l > 0.f ? 1.0f / l : 0.f;
       T* dst = reinterpret_cast<T*>(a.o) + ((long long)a.q_rowbase[b] + qs) * a.ldo + head * HD;
 #pragma unroll
-      for (int d = 0; d < HD; d += 8) {
-        float v[8];
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(o_addr + c * 32, r);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = o[d + i] * inv;
-        store16<T>(dst + d, v);
+        for (int d = 0; d < 32; d += 8) {
+          float v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[d + i]) * inv;
+          store16<T>(dst + c * 32 + d, v);
+        }
       }
     }
   }
   __syncthreads();
-  if (warp == 1) {
+  if (warp == NSM + 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -290,7 +312,6 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   a.heads = p.heads;
   a.smax = (int)(p.k_sh / p.hd);
   a.causal = p.causal;
-  a.scale = p.scale;
   a.scale_log2 = p.scale * 1.4426950408889634f;
   auto kern = attn_tc_kernel<T, HD>;
   static bool attr = false;
@@ -298,7 +319,7 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  dim3 grid((p.seq + BQ - 1) / BQ, p.heads, p.batch);
+  dim3 grid((p.seq + 2 * BQ - 1) / (2 * BQ), p.heads, p.batch);
   ProfScope ps(K_ATTN_PREFILL, st, bytes, flops);
   kern<<<grid, THREADS, C::SMEM, st>>>(mq, mk, mv, a);
   EET_LAUNCH_CHECK();
