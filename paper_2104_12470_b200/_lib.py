@@ -13,6 +13,10 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libeet_b200.so")
+# development only: a debug build (mbarrier watchdog) built with
+# `python -m paper_2104_12470_b200.build --debug`
+if os.environ.get("EET_DEBUG_LIB") == "1":
+    LIB_PATH = os.path.join(_HERE, "libeet_b200_dbg.so")
 
 EET_OK, EET_ERR_SHAPE, EET_ERR_OVERFLOW, EET_ERR_CUDA, EET_ERR_POOL, EET_ERR_ARG, EET_ERR_UNSUPPORTED = range(7)
 EET_F32, EET_BF16, EET_F16 = 0, 1, 2

@@ -36,39 +36,43 @@ def _mtime(p):
         return 0.0
 
 
-def _compile(src: str, force: bool) -> str:
+def _compile(src: str, force: bool, debug: bool = False) -> str:
     s = os.path.join(CSRC, src)
-    o = os.path.join(BUILD, src.replace(".cu", ".o"))
+    o = os.path.join(BUILD + ("_dbg" if debug else ""), src.replace(".cu", ".o"))
     deps = [s] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "eet_b200.h")]
     if not force and _mtime(o) > max(_mtime(d) for d in deps):
         return o
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+    cmd = [NVCC, *ARCH, *FLAGS, *(["-DEET_WATCHDOG"] if debug else []), "-c", s, "-o", o]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return o
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = True, debug: bool = False) -> str:
+    """debug=True builds libeet_b200_dbg.so with the mbarrier watchdog
+    (loaded only when EET_DEBUG_LIB=1)."""
+    lib = LIB.replace(".so", "_dbg.so") if debug else LIB
+    os.makedirs(BUILD + ("_dbg" if debug else ""), exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
-    if force or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
+        objs = list(ex.map(lambda s: _compile(s, force, debug), SOURCES))
+    if force or _mtime(lib) < max(_mtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         if verbose:
-            print(f"built {LIB}")
-    return LIB
+            print(f"built {lib}")
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--debug", action="store_true")
     a = ap.parse_args()
     try:
-        build(force=a.force)
+        build(force=a.force, debug=a.debug)
     except RuntimeError as e:
         print(e, file=sys.stderr)
         sys.exit(1)

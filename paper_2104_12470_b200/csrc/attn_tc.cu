@@ -233,21 +233,25 @@ __global__ void __launch_bounds__(THREADS, 1)
       // O rows and P buffer of tile j-1 must be done before we touch them
       if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);
       tc_fence_after();
-      if (tmax > m + RESCALE_LOG2 || (m == -INFINITY && tmax != -INFINITY)) {
+      // tcgen05.ld/st are .sync.aligned: the O rescale is decided per warp
+      // (any row whose max grew past the threshold rescales the whole warp;
+      // rescaling a row that did not need it is exact up to rounding)
+      const bool need = tmax > m + RESCALE_LOG2 || (m == -INFINITY && tmax != -INFINITY);
+      if (__any_sync(0xffffffffu, need && m != -INFINITY)) {
         const float m_new = fmaxf(m, tmax);
-        if (m != -INFINITY) {                             // rescale O and l
-          const float f = exp2f(m - m_new);
-          l *= f;
+        const float f = (m == -INFINITY) ? 1.f : exp2f(m - m_new);   // -inf row: O is still zero
+        l *= f;
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(o_addr + c * 32, r);
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(o_addr + c * 32, r);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-            tmem_st32(o_addr + c * 32, r);
-          }
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+          tmem_st32(o_addr + c * 32, r);
         }
         m = m_new;
+      } else if (need) {
+        m = tmax;                                         // first live tile of this row
       }
       const float msub = (m == -INFINITY) ? 0.f : m;
       float rs = 0.f;
@@ -270,19 +274,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (ntile > 0) mbar_wait(&o_done[t], (ntile - 1) & 1);
     tc_fence_after();
-    if (live && ntile > 0) {
+    if (ntile > 0) {                                      // warp-uniform TMEM reads
       const float inv = l > 0.f ? 1.0f / l : 0.f;
       T* dst = reinterpret_cast<T*>(a.o) + ((long long)a.q_rowbase[b] + qs) * a.ldo + head * HD;
 #pragma unroll
       for (int c = 0; c < HD / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(o_addr + c * 32, r);
+        if (live) {
 #pragma unroll
-        for (int d = 0; d < 32; d += 8) {
-          float v[8];
+          for (int d = 0; d < 32; d += 8) {
+            float v[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[d + i]) * inv;
-          store16<T>(dst + c * 32 + d, v);
+            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[d + i]) * inv;
+            store16<T>(dst + c * 32 + d, v);
+          }
         }
       }
     }

@@ -64,7 +64,15 @@ struct Fail {
     }                                                                          \
   } while (0)
 
-#define EET_LAUNCH_CHECK() EET_CHECK_CUDA(cudaGetLastError())
+// EET_SYNC_DEBUG=1: synchronise after every launch and name it on stderr
+// (locates a hanging or faulting kernel; never set during timing).
+bool sync_debug();
+void sync_debug_after(const char* file, int line);
+#define EET_LAUNCH_CHECK()                                                     \
+  do {                                                                         \
+    EET_CHECK_CUDA(cudaGetLastError());                                        \
+    if (::eet::sync_debug()) ::eet::sync_debug_after(__FILE__, __LINE__);      \
+  } while (0)
 
 // ------------------------------------------------------------ folding plan
 // folding.py:30-54: minimal k with ceil(n / 2^k) <= cap.

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -16,6 +17,27 @@ namespace eet {
 static thread_local std::string t_err;
 std::atomic<uint64_t> g_launches{0};
 void set_error(const std::string& msg) { t_err = msg; }
+
+bool sync_debug() {
+  static const bool on = [] {
+    const char* e = std::getenv("EET_SYNC_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+void sync_debug_after(const char* file, int line) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(nullptr, &cs);
+  std::fprintf(stderr, "[eet] launch %s:%d ... ", file, line);
+  std::fflush(stderr);
+  if (cs == cudaStreamCaptureStatusNone) {
+    const cudaError_t e = cudaDeviceSynchronize();
+    std::fprintf(stderr, "%s\n", cudaGetErrorString(e));
+  } else {
+    std::fprintf(stderr, "(capturing)\n");
+  }
+  std::fflush(stderr);
+}
 
 // ------------------------------------------------------------ profiler
 namespace {

@@ -1,0 +1,25 @@
+#!/bin/bash
+# ncu evidence for profiles/: launch lists (per-launch duration, cold-cache,
+# serialised) of the c2 generate path and the c3/c4 layers, plus one
+# `--set full` capture of each dominant kernel. Run under gpurun on ONE GPU:
+#   gpurun --timeout 1800 -- 'bash tools/ncu_round.sh'
+# Outputs land in gpurun_out/ncu/ (scratch); summaries are copied to profiles/.
+set -x
+O=gpurun_out/ncu
+mkdir -p $O
+NCU=ncu
+LIST="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv"
+FULL="--set full --clock-control none --import-source on"
+
+timeout 900 $NCU $LIST --log-file $O/launches_c2.csv python tools/decode_profile.py --steps 4 > $O/launches_c2.log 2>&1
+for w in c3 c4 c5; do
+  timeout 600 $NCU $LIST --log-file $O/launches_$w.csv python tools/layer_profile.py --workload $w > $O/launches_$w.log 2>&1
+done
+
+# full captures of the top kernels (skip the warm-up call's launches)
+timeout 600 $NCU $FULL -k regex:gemv_tc -s 400 -c 4 -o $O/gemv_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_c2.log 2>&1
+timeout 600 $NCU $FULL -k regex:attn_decode -s 60 -c 2 -o $O/attn_decode_c2 -f python tools/decode_profile.py --steps 4 > $O/attn_decode_c2.log 2>&1
+timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c3 -f python tools/layer_profile.py --workload c3 > $O/attn_tc_c3.log 2>&1
+timeout 600 $NCU $FULL -k regex:gemm_tc -s 4 -c 4 -o $O/gemm_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/gemm_tc_c4.log 2>&1
+timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/attn_tc_c4.log 2>&1
+ls -la $O
