@@ -84,6 +84,119 @@ __global__ void __launch_bounds__(1024) ln_kernel(
   }
 }
 
+// Row-group LayerNorm for the layer path: W warps own one row (folded into
+// NV float4 sub-blocks per lane, the same folding as above with a fixed
+// 32*W-lane unit), 8/W rows per 256-thread CTA, warp-shuffle reductions,
+// float4 loads of x / gamma / beta and 8-16 B packed stores. Two-pass
+// statistics (mean, then centred second moment) as numpy.
+template <int W>
+__device__ __forceinline__ float row_sum(float v, float (*red)[2], int slot, int warp, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if constexpr (W == 1) {
+    return v;
+  } else {
+    if (lane == 0) red[warp][slot] = v;
+    __syncthreads();
+    const int base = (warp / W) * W;
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) t += red[base + w][slot];
+    return t;
+  }
+}
+
+template <typename TO, int W, int NV>
+__global__ void __launch_bounds__(256) ln_rows_kernel(
+    const float* __restrict__ x, long long x_sb, long long x_ss, const int2* __restrict__ rinfo,
+    const float* __restrict__ g, const float* __restrict__ b, TO* __restrict__ y, int ldy, int h,
+    int rows) {
+  __shared__ float red[8][2];
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (8 / W) + warp / W;
+  const int tid = (warp % W) * 32 + lane;
+  const bool active = r < rows;
+  const float* xr = x;
+  if (active) {
+    if (rinfo) {
+      const int2 ri = rinfo[r];
+      xr = x + ri.x * x_sb + ri.y * x_ss;
+    } else {
+      xr = x + (long long)r * x_sb;
+    }
+  }
+  const int nvec = h >> 2;
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int idx = i * 32 * W + tid;
+    v[i] = (active && idx < nvec) ? __ldg(reinterpret_cast<const float4*>(xr) + idx)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+  const float mean = row_sum<W>(s, red, 0, warp, lane) / (float)h;
+  float q2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int idx = i * 32 * W + tid;
+    if (active && idx < nvec) {
+      const float a = v[i].x - mean, c = v[i].y - mean, d = v[i].z - mean, e = v[i].w - mean;
+      q2 += (a * a + c * c) + (d * d + e * e);
+    }
+  }
+  const float rstd = 1.0f / sqrtf(row_sum<W>(q2, red, 1, warp, lane) / (float)h + 1e-5f);
+  if (!active) return;
+  TO* yr = y + (long long)r * ldy;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int idx = i * 32 * W + tid;
+    if (idx >= nvec) continue;
+    const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + idx);
+    const float4 bb = __ldg(reinterpret_cast<const float4*>(b) + idx);
+    const float o0 = (v[i].x - mean) * rstd * gg.x + bb.x;
+    const float o1 = (v[i].y - mean) * rstd * gg.y + bb.y;
+    const float o2 = (v[i].z - mean) * rstd * gg.z + bb.z;
+    const float o3 = (v[i].w - mean) * rstd * gg.w + bb.w;
+    if constexpr (sizeof(TO) == 4) {
+      reinterpret_cast<float4*>(yr)[idx] = make_float4(o0, o1, o2, o3);
+    } else {
+      TO t[4] = {from_f<TO>(o0), from_f<TO>(o1), from_f<TO>(o2), from_f<TO>(o3)};
+      reinterpret_cast<uint2*>(yr)[idx] = *reinterpret_cast<const uint2*>(t);
+    }
+  }
+}
+
+// rows kernel when the shape allows (h % 4, 16-byte aligned rows, output
+// rows 8/16-byte aligned); returns false otherwise
+template <typename TO>
+static bool ln_rows_dispatch(const float* x, long long x_sb, long long x_ss, const int2* rinfo,
+                             int rows, const float* g, const float* b, TO* y, int ldy, int h,
+                             cudaStream_t st) {
+  const uintptr_t al = reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) |
+                       reinterpret_cast<uintptr_t>(b);
+  if (h % 4 || (al & 15) || (x_ss & 3) || (x_sb & 3) || (!rinfo && x_sb == 0) ||
+      (ldy % 4) || (reinterpret_cast<uintptr_t>(y) & (sizeof(TO) * 4 - 1)))
+    return false;
+  const int nvec = h / 4;
+  int W = 1;
+  while (W < 8 && (nvec + 32 * W - 1) / (32 * W) > 8) W *= 2;
+  const int nv = (nvec + 32 * W - 1) / (32 * W);
+  ProfScope ps(K_LAYERNORM, st, (double)rows * h * (4 + sizeof(TO)) + 8.0 * h, 8.0 * rows * h);
+#define LNR(W_, NV_)                                                                          \
+  if (W == W_ && nv <= NV_) {                                                                 \
+    launch_ex(ln_rows_kernel<TO, W_, NV_>, dim3((rows + 8 / W_ - 1) / (8 / W_)), dim3(256), 0, st, \
+              true, dim3(1, 1, 1), x, x_sb, x_ss, rinfo, g, b, y, ldy, h, rows);             \
+    EET_LAUNCH_CHECK();                                                                       \
+    return true;                                                                              \
+  }
+  LNR(1, 2) LNR(1, 4) LNR(1, 8) LNR(2, 8) LNR(4, 8) LNR(8, 8) LNR(8, 12) LNR(8, 16)
+#undef LNR
+  return false;
+}
+
 template <typename TO, int VEC>
 static void ln_dispatch(const float* x, long long x_sb, long long x_ss, const int2* rinfo, int rows,
                         const float* g, const float* b, TO* y, int ldy, int h, int cap,
@@ -109,6 +222,13 @@ void launch_layer_norm(const float* x, long long x_sb, long long x_ss, const int
                        int h, int cap, cudaStream_t st) {
   if (rows <= 0) return;
   EET_REQUIRE(h >= 1 && h <= 16384, EET_ERR_ARG, "layer norm: hidden outside [1, 16384]");
+  if (cap == 0) {          // layer path: row-group kernel; explicit fold caps keep the folded CTA shape
+    const bool done =
+        y_dtype == EET_F32    ? ln_rows_dispatch(x, x_sb, x_ss, rinfo, rows, g, b, (float*)y, ldy, h, st)
+        : y_dtype == EET_BF16 ? ln_rows_dispatch(x, x_sb, x_ss, rinfo, rows, g, b, (__nv_bfloat16*)y, ldy, h, st)
+                              : ln_rows_dispatch(x, x_sb, x_ss, rinfo, rows, g, b, (__half*)y, ldy, h, st);
+    if (done) return;
+  }
   bool v4 = (h % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) &&
             (x_ss % 4 == 0) && (x_sb % 4 == 0) && (rinfo || x_sb != 0);
   switch (y_dtype) {
