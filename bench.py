@@ -61,7 +61,7 @@ WORKLOADS = {
                lengths="full", desc="decoder layer h12288 96 heads s2048 b1, bf16"),
 }
 
-HBM_KINDS = {"attn_decode", "gemv", "layernorm", "embed", "argmax", "softmax", "advance"}
+HBM_KINDS = {"attn_decode", "gemv", "layernorm", "embed", "argmax", "softmax", "advance", "decode_step"}
 
 
 def peaks():

@@ -52,6 +52,12 @@ typedef enum { EET_PHASE_PROMPT = 0, EET_PHASE_INCREMENTAL = 1 } eet_phase;
 /* ---------------------------------------------------------------- library */
 const char* eet_last_error(void);
 int eet_abi_version(void);
+
+/* Selects the decode path of eet_generate for eligible shapes (16-bit, head
+ * dim 64, h <= 2048, batch <= 16): 1 = persistent decode megakernel (one
+ * launch per step), 0 = per-op kernels in a CUDA graph (default). Returns
+ * the previous setting. New; the reference has a single CPU path. */
+int eet_set_decode_megakernel(int on);
 /* Number of kernel launches issued by this library since load (the bench's
  * gpu_launches evidence). */
 uint64_t eet_launch_count(void);
@@ -127,6 +133,13 @@ int eet_mha_forward(const float* q, const float* k, const float* v, float* out,
  * C is float32 [M, ldc]. Used by tests and the LM head. */
 int eet_gemm(int dtype, const void* A, const void* B, const float* bias,
              float* C, int M, int N, int K, int ldc, void* stream);
+
+/* Decode GEMV through the packed-fragment path (gemv_mma.cu): packs W
+ * [N, K] (K-major, 16-bit) and computes out[M, N] = X[M, K] W^T in fp32,
+ * M <= 16. repack = 0 reuses the copy packed by an earlier call for the same
+ * w. Test / micro-benchmark entry; generate uses the path internally. */
+int eet_gemv_packed(int dtype, const void* w, int N, int K, const void* X, int M,
+                    float* out, int repack, void* stream);
 
 /* ------------------------------------------------------------ layer path */
 typedef struct {

@@ -57,6 +57,8 @@ SIGNATURES = {
     "eet_profile_enable": (i32, [i32]),
     "eet_profile_kinds": (i32, []),
     "eet_profile_kind_name": (C.c_char_p, [i32]),
+    "eet_set_decode_megakernel": (i32, [i32]),
+    "eet_gemv_packed": (i32, [i32, p, i32, i32, p, i32, p, i32, p]),
     "eet_profile_summary": (i32, [i32, C.POINTER(u64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "eet_plan_folding": (i32, [i32, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
     "eet_pool_create": (i32, [C.POINTER(p)]),
@@ -154,3 +156,10 @@ def profile_summary() -> dict:
         if n.value:
             out[L.eet_profile_kind_name(k).decode()] = (n.value, ms.value, by.value, fl.value)
     return out
+
+
+def set_decode_megakernel(on: bool) -> bool:
+    """Decode path of generate for eligible shapes: True = persistent
+    megakernel (default), False = per-op kernels in a CUDA graph. Returns the
+    previous setting."""
+    return bool(lib().eet_set_decode_megakernel(1 if on else 0))

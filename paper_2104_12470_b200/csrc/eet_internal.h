@@ -24,7 +24,7 @@ inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_o
 // tagged with its algorithmic bytes / flops. Also counts every launch.
 enum KernelKind : int {
   K_LAYERNORM = 0, K_SOFTMAX, K_EMBED, K_ARGMAX, K_ADVANCE, K_GEMM_F32, K_GEMV,
-  K_GEMM_TC, K_ATTN_PREFILL, K_ATTN_DECODE, K_KIND_COUNT
+  K_GEMM_TC, K_ATTN_PREFILL, K_ATTN_DECODE, K_DECODE_STEP, K_KIND_COUNT
 };
 struct ProfScope {
   int slot = -1;
@@ -186,6 +186,28 @@ struct DecodeArgs {
   int splits;
 };
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
+int decode_range_ctas();               // CTAs of the key-range decode kernel (part: 2 slots each)
+
+// ---- decode GEMV from pre-permuted weights (gemv_mma.cu)
+void packed_register(const void* src, const void* packed);
+void packed_clear();
+bool gemv_packed(int dtype, const void* wsrc, int M, int N, int K, const void* X, int ldx,
+                 const float* x, long long x_sb, long long x_ss, const int2* rinfo, const float* g,
+                 const float* b, const Epi& e, cudaStream_t st);
+
+// ---- persistent decode megakernel (decode_mk.cu)
+struct MkState;
+void mk_state_free(MkState* s);
+bool mk_eligible(int dtype, int h, int heads, int batch, int ffn);
+size_t mk_packed_bytes(int N, int K);
+void mk_pack(const void* w, int N, int K, void* out, cudaStream_t st);
+// pack every projection of the model (and the LM head) into st's buffer and
+// register the copies for gemv_packed
+void mk_pack_model(MkState*& st, int dtype, const eet_model* m, int h, cudaStream_t stream);
+void mk_generate(MkState*& st, int dtype, int h, int heads, int bmax, int smax,
+                 const eet_model* m, int batch, const int* d_pads, const int* h_pads, int t,
+                 int* d_filled, int* d_step, int* d_cur, long long* d_tokens, int steps,
+                 float* d_logits, cudaStream_t stream);
 int decode_splits(int batch, int heads, int smax, int hd, int es);
 
 // cudaLaunchKernelEx with optional programmatic-dependent-launch edge and

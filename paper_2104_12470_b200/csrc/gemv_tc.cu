@@ -28,6 +28,8 @@
 // stream in while the previous kernel is still finishing.
 #include "sm100.cuh"
 
+#include <map>
+
 namespace eet {
 namespace gv {
 using namespace sm100;
@@ -271,15 +273,46 @@ __global__ void __launch_bounds__(THREADS) gemv_tc_kernel(
   cluster_sync();                       // peers may still be reading our slice
 }
 
-// splits: ~2 CTAs per SM, <= 8 per cluster, every split non-empty; LNX keeps
-// the whole K-range of a CTA in shared memory (<= MAX_KBPS k-blocks).
-static void plan_splits(int rbs, int nkb, bool lnx, int* splits, int* kbps) {
+// splits: ~2 CTAs per SM, <= 8 per cluster, every split non-empty, and all
+// clusters co-resident (one wave): ncu r01 showed 8-CTA clusters capped at 15
+// active clusters, i.e. 3 waves for the QKV / W1 shapes. `max_clusters(s)`
+// is the occupancy query for cluster size s. LNX keeps the whole K-range of
+// a CTA in shared memory (<= MAX_KBPS k-blocks).
+template <typename F>
+static void plan_splits(int rbs, int nkb, bool lnx, int* splits, int* kbps, F max_clusters) {
   const int target = 2 * device_sm_count();
   int s = std::min(std::max(1, (target + rbs - 1) / rbs), std::min(nkb, 8));
+  while (s > 1 && rbs > max_clusters(s)) --s;
   if (lnx) s = std::max(s, (nkb * BK + LNX_MAX_COLS - 1) / LNX_MAX_COLS);
   const int k = (nkb + s - 1) / s;
   *kbps = k;
   *splits = (nkb + k - 1) / k;
+}
+
+template <typename Kern>
+static int active_clusters(Kern kern, int smem, int s) {
+  static std::map<std::pair<const void*, int>, int> cache;   // (kernel, s)
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), s);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1, s, 1);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = s;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 2 * device_sm_count() / s;
+  }
+  cache[key] = n;
+  return n;
 }
 
 template <typename T, int MN, bool LNX>
@@ -288,17 +321,18 @@ static void launch(const void* A, int lda, const LnSrc& ln, const void* B, int l
   using L = Lay<MN, LNX>;
   const int rbs = (N + ROWS - 1) / ROWS;
   const int nkb = (K + BK - 1) / BK;
-  int splits, kbps;
-  plan_splits(rbs, nkb, LNX, &splits, &kbps);
-  EET_REQUIRE(splits <= 8, EET_ERR_UNSUPPORTED, "gemv_tc: K too long for one cluster");
-  CUtensorMap mw = make_tma_map_2d(B, N, K, ldb, ROWS, dtype);
-  CUtensorMap mx = LNX ? mw : make_tma_map_2d(A, M, K, lda, MN, dtype);
   auto kern = gemv_tc_kernel<T, MN, LNX>;
   static bool attr = false;
   if (!attr) {
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
+    EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
+  int splits, kbps;
+  plan_splits(rbs, nkb, LNX, &splits, &kbps, [&](int s) { return active_clusters(kern, L::SMEM, s); });
+  EET_REQUIRE(splits <= 8, EET_ERR_UNSUPPORTED, "gemv_tc: K too long for one cluster");
+  CUtensorMap mw = make_tma_map_2d(B, N, K, ldb, ROWS, dtype);
+  CUtensorMap mx = LNX ? mw : make_tma_map_2d(A, M, K, lda, MN, dtype);
   const double xbytes = LNX ? (double)M * K * 4 : (double)M * K * 2;
   ProfScope ps(K_GEMV, st, gemm_bytes(M, N, K, 2, e) - (double)M * K * 2 + xbytes, 2.0 * M * N * K);
   launch_ex(kern, dim3(rbs, splits), dim3(THREADS), L::SMEM, st, true, dim3(1, splits, 1), mw, mx,
@@ -334,7 +368,12 @@ bool gemv_tc_ln_sm100(int dtype, const float* x, long long x_sb, long long x_ss,
     return false;
   {
     int sp, kb;
-    gv::plan_splits((N + gv::ROWS - 1) / gv::ROWS, K / 64, false, &sp, &kb);
+    auto kern = dtype == EET_BF16 ? (M <= 16 ? gv::gemv_tc_kernel<__nv_bfloat16, 16, true> : gv::gemv_tc_kernel<__nv_bfloat16, 32, true>)
+                                  : (M <= 16 ? gv::gemv_tc_kernel<__half, 16, true> : gv::gemv_tc_kernel<__half, 32, true>);
+    const int smem = M <= 16 ? gv::Lay<16, true>::SMEM : gv::Lay<32, true>::SMEM;
+    EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    gv::plan_splits((N + gv::ROWS - 1) / gv::ROWS, K / 64, false, &sp, &kb,
+                    [&](int s) { return gv::active_clusters(kern, smem, s); });
     if (kb * 64 > gv::LNX_MAX_COLS) return false;       // e.g. LM head: 1 split of 1024 columns
   }
   const gv::LnSrc ln{x, x_sb, x_ss, rinfo, g, b};

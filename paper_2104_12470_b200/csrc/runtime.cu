@@ -69,7 +69,7 @@ struct Profiler {
 
 const char* kKindNames[K_KIND_COUNT] = {"layernorm", "softmax", "embed", "argmax", "advance",
                                         "gemm_f32", "gemv", "gemm_tc", "attn_prefill",
-                                        "attn_decode"};
+                                        "attn_decode", "decode_step"};
 
 void fold(const ProfRec& r, double keys) {
   float e = 0.f;
@@ -135,10 +135,33 @@ using namespace eet;
 
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Development ablation: EET_SKIP=qkv,attn,o,w1,w2,head skips those decode
+// launches (results become wrong; used only to time their in-graph cost).
+static bool skip_decode(const char* what) {
+  static const std::string spec = [] {
+    const char* e = std::getenv("EET_SKIP");
+    return std::string(e ? e : "");
+  }();
+  if (spec.empty()) return false;
+  return ("," + spec + ",").find("," + std::string(what) + ",") != std::string::npos;
+}
+
+// decode megakernel switch (default off: EET_MEGAKERNEL=1 or eet_set_decode_megakernel)
+static std::atomic<int> g_decode_mk{[] {
+  const char* e = std::getenv("EET_MEGAKERNEL");
+  return (e && e[0] == '1') ? 1 : 0;
+}()};
+
 extern "C" {
 
 const char* eet_last_error(void) { return t_err.c_str(); }
 int eet_abi_version(void) { return 1; }
+
+int eet_set_decode_megakernel(int on) {
+  const int prev = g_decode_mk.load();
+  g_decode_mk.store(on != 0);
+  return prev;
+}
 uint64_t eet_launch_count(void) { return g_launches.load(); }
 
 int eet_profile_enable(int on) {
@@ -457,6 +480,7 @@ struct eet_runtime {
   int* d_cur = nullptr;               // [bmax]
   int* h_prompts = nullptr;           // pinned staging: prompts in, tokens out
   long long* h_tokens = nullptr;
+  MkState* mk = nullptr;              // decode megakernel state (packed weights, scratch)
 
   void* dev(size_t bytes) {
     void* p = nullptr;
@@ -465,6 +489,7 @@ struct eet_runtime {
     return p;
   }
   ~eet_runtime() {
+    if (mk) mk_state_free(mk);
     for (void* p : owned) cudaFree(p);
     if (h_prompts) cudaFreeHost(h_prompts);
     if (h_tokens) cudaFreeHost(h_tokens);
@@ -543,8 +568,13 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     e.kv_start = kv_dev;
     e.kv_base = kv_base;
     // decode rows: LN1 runs inside the GEMV prologue; otherwise LN -> GEMM
-    if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b, w->wqkv, h,
-                                      T, 3 * hq, h, e, st))) {
+    const bool inc = p.phase == EET_PHASE_INCREMENTAL;
+    if (inc && skip_decode("qkv")) {
+    } else if (inc && gemv_packed(dt, w->wqkv, T, 3 * hq, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln1_g,
+                           w->ln1_b, e, st)) {
+      // packed-weight decode GEMV with the LayerNorm fused (gemv_mma.cu)
+    } else if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b, w->wqkv, h,
+                                             T, 3 * hq, h, e, st))) {
       Claim ln(rt->pool, (size_t)T * h * es, scope, "attention.layernorm");
       launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln1_g, w->ln1_b, ln.ptr, dt, h, h, 0, st);
       gemm(dt, ln.ptr, h, w->wqkv, h, T, 3 * hq, h, e, st);
@@ -586,7 +616,7 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     a.counters = rt->counters;
     a.o = ctx.ptr; a.ldo = hq;
     a.splits = rt->splits;
-    launch_attn_decode(a, st);
+    if (!skip_decode("attn")) launch_attn_decode(a, st);
   }
   q.release();
   {
@@ -601,7 +631,10 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
       e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
       e.rinfo = p.rinfo;
     }
-    gemm(dt, ctx.ptr, hq, w->wo, hq, T, h, hq, e, st);
+    if (p.phase == EET_PHASE_INCREMENTAL && skip_decode("o")) {
+    } else if (!(p.phase == EET_PHASE_INCREMENTAL &&
+          gemv_packed(dt, w->wo, T, h, hq, ctx.ptr, hq, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
+      gemm(dt, ctx.ptr, hq, w->wo, hq, T, h, hq, e, st);
   }
   ctx.release();
 }
@@ -621,8 +654,12 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
     e.bias = w->b_1;
     e.out = mid.ptr;
     e.ldo = f;
-    if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T,
-                                      f, h, e, st))) {
+    const bool inc = p.phase == EET_PHASE_INCREMENTAL;
+    if (inc && skip_decode("w1")) {
+    } else if (inc && gemv_packed(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b,
+                           e, st)) {
+    } else if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T,
+                                             f, h, e, st))) {
       Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
       launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln2_g, w->ln2_b, ln2.ptr, dt, h, h, 0, st);
       gemm(dt, ln2.ptr, h, w->w1, h, T, f, h, e, st);
@@ -640,7 +677,10 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
       e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
       e.rinfo = p.rinfo;
     }
-    gemm(dt, mid.ptr, f, w->w2, f, T, h, f, e, st);
+    if (p.phase == EET_PHASE_INCREMENTAL && skip_decode("w2")) {
+    } else if (!(p.phase == EET_PHASE_INCREMENTAL &&
+          gemv_packed(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
+      gemm(dt, mid.ptr, f, w->w2, f, T, h, f, e, st);
   }
   mid.release();
 }
@@ -681,7 +721,9 @@ static eet_runtime* runtime_new(int dtype, int hidden, int heads_total, int tp_r
   rt->pool = pool;
   rt->splits = decode_splits(max_batch, heads, max_sequence, rt->hd, (int)dtype_size(dtype));
   for (auto& p : rt->plans) plan_alloc(rt.get(), p);
-  rt->part = (float*)rt->dev(sizeof(float) * (size_t)max_batch * heads * rt->splits * (rt->hd + 2));
+  rt->part = (float*)rt->dev(sizeof(float) *
+                             std::max((size_t)max_batch * heads * rt->splits, (size_t)2 * decode_range_ctas()) *
+                             (rt->hd + 2));
   rt->counters = (int*)rt->dev(sizeof(int) * (size_t)max_batch * heads);
   EET_CHECK_CUDA(cudaMemset(rt->counters, 0, sizeof(int) * (size_t)max_batch * heads));
   rt->d_prompts = (int*)rt->dev(sizeof(int) * (size_t)max_batch * max_sequence);
@@ -817,8 +859,10 @@ static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long 
   e.ldo = m->vocab;
   // rows (b, slot): the decode plan's row map (b, 0) over x shifted by `slot`
   const float* xs = x + (long long)slot * h;
-  if (!(batch <= 32 && gemv_tc_ln_sm100(dt, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g, m->lnf_b,
-                                        m->head, h, batch, m->vocab, h, e, st))) {
+  if (gemv_packed(dt, m->head, batch, m->vocab, h, nullptr, 0, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g,
+                  m->lnf_b, e, st)) {
+  } else if (!(batch <= 32 && gemv_tc_ln_sm100(dt, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g, m->lnf_b,
+                                               m->head, h, batch, m->vocab, h, e, st))) {
     Claim ln(rt->pool, (size_t)batch * h * es, EET_SCOPE_ACROSS, "output.layernorm");
     launch_layer_norm(xs, x_sb, h, nullptr, batch, m->lnf_g, m->lnf_b, ln.ptr, dt, h, h, 0, st);
     gemm(dt, ln.ptr, h, m->head, h, batch, m->vocab, h, e, st);
@@ -888,10 +932,25 @@ int eet_generate(eet_runtime* rt, const eet_model* m, const int* h_prompts, cons
     EET_CHECK_CUDA(cudaMemcpyAsync(rt->d_step, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
     StepPlan& ps = rt->plans[2];
     plan_fill(ps, batch, 1, pads.data(), t, EET_PHASE_INCREMENTAL, st);
+    const bool use_mk = g_decode_mk.load() && rt->tp_size == 1 && mk_eligible(rt->dtype, h, rt->heads, batch, rt->ffn);
+    // decode projections from packed weights (gemv_mma.cu), registered for
+    // this call only
+    struct PackGuard {
+      ~PackGuard() { packed_clear(); }
+    } pack_guard;
+    if (!use_mk && rt->tp_size == 1 && (rt->dtype == EET_F16 || rt->dtype == EET_BF16) && batch <= 16 &&
+        rt->ffn == 4 * h && h % 16 == 0)
+      mk_pack_model(rt->mk, rt->dtype, m, h, st);
     head_step(rt, m, m->hidden, x_sb, t - 1, batch, steps, tok.as<long long>(), d_logits, st);
+    if (use_mk) {
+      // persistent megakernel: one launch per decode step (decode_mk.cu)
+      mk_generate(rt->mk, rt->dtype, h, rt->heads, rt->bmax, rt->smax, m, batch, ps.pads, pads.data(),
+                  t, rt->d_filled, rt->d_step, rt->d_cur, tok.as<long long>(), steps, d_logits, st);
+    } else {
     // step 0 eagerly (settles every pool buffer), the rest replay one graph
     decode_iteration(rt, m, batch, steps, tok.as<long long>(), d_logits, t + 1, st);
-    if (steps > 1) {
+    }
+    if (steps > 1 && !use_mk) {
       if (use_graph) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
