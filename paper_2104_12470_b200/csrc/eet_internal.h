@@ -89,6 +89,7 @@ enum EpiMode : int {
   EPI_GELU_T = 2,     // out_T[m*ldo + n]   = gelu(acc + bias)
   EPI_RESID = 3,      // x[b*x_sb + t*x_ss + n] += acc + bias      (row map)
   EPI_QKV = 4,        // n<hq: q_T[m*hq+n]; else K/V cache scatter (row map)
+  EPI_ARGMAX = 5,     // LM head: greedy token per row (gemv_packed only), optional logits
 };
 
 struct Epi {
@@ -106,6 +107,14 @@ struct Epi {
   int heads = 0, hd = 0, hq = 0, smax = 0;
   const int* kv_start = nullptr;  // device scalar (may be null) ...
   int kv_base = 0;                // ... plus this: first cache slot of the step
+  // EPI_ARGMAX (runtime.py:425: lowest id on ties); out = optional logits
+  // [steps, batch, vocab] written at step *d_step
+  int2* cand = nullptr;           // [rtiles * 16] (value bits, id) per tile and row
+  int* ticket = nullptr;          // zero on entry, left zero
+  int* cur = nullptr;             // [batch] next token
+  long long* toks = nullptr;      // [batch, steps]
+  const int* d_step = nullptr;
+  int steps = 0, batch = 0;
 };
 
 // ---------------------------------------------------------------- launchers

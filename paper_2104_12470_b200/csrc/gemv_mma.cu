@@ -59,6 +59,86 @@ __device__ __forceinline__ void mma16816(float* d, const uint4& a, uint32_t b0, 
   }
 }
 
+// LM-head epilogue: greedy token per row (np.argmax, lowest id on ties,
+// runtime.py:425). Each CTA reduces its 16 vocab rows per token into a
+// candidate; the CTA that finishes last (acq_rel ticket) reduces all
+// candidates — 16 threads per token, candidate ranges in id order — and
+// records the token (argmax_kernel's job, without a logits round trip).
+__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+template <typename T>
+__device__ __noinline__ void argmax_tail(const Args<T>& a, const float* red, int NB) {
+  __shared__ float tile[16][17];
+  __shared__ float bvs[16][16];
+  __shared__ int bis[16][16];
+  __shared__ int s_last;
+  const Epi& e = a.e;
+  const int rt = blockIdx.x;
+  const int step = *e.d_step;
+  for (int t = threadIdx.x; t < 256; t += blockDim.x) tile[t >> 4][t & 15] = -INFINITY;
+  __syncthreads();
+  if (threadIdx.x < NB * 128) {
+    const int el = threadIdx.x;
+    float v = 0.f;
+    for (int w = 0; w < WARPS; ++w) v += red[(w * NB * 4) * 32 + el];
+    const int i = el >> 5, ln = el & 31;
+    const int row = (ln >> 2) + 8 * ((i & 3) >> 1);
+    const int tok = (i >> 2) * 8 + 2 * (ln & 3) + (i & 1);
+    const int n = rt * 16 + row;
+    if (n < a.N && tok < a.M) {
+      tile[tok][row] = v;
+      if (e.out && step < e.steps)
+        reinterpret_cast<float*>(e.out)[((long long)step * e.batch + tok) * e.ldo + n] = v;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < a.M) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int r = 0; r < 16; ++r)
+      if (rt * 16 + r < a.N && better(tile[threadIdx.x][r], rt * 16 + r, bv, bi)) {
+        bv = tile[threadIdx.x][r];
+        bi = rt * 16 + r;
+      }
+    e.cand[rt * 16 + threadIdx.x] = make_int2(__float_as_int(bv), bi);
+  }
+}
+
+// second stage: one CTA per token reduces the per-tile candidates in id order
+__global__ void __launch_bounds__(256) argmax_cand_kernel(const int2* __restrict__ cand, int rtiles,
+                                                          int* __restrict__ cur, long long* __restrict__ toks,
+                                                          int steps, const int* __restrict__ d_step) {
+  __shared__ float sv[8];
+  __shared__ int si[8];
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
+  const int tok = blockIdx.x;
+  const int per = (rtiles + 255) / 256;
+  float bv = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int r = threadIdx.x * per; r < min(rtiles, (threadIdx.x + 1) * per); ++r) {
+    const int2 c = cand[r * 16 + tok];
+    if (better(__int_as_float(c.x), c.y, bv, bi)) { bv = __int_as_float(c.x); bi = c.y; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = bv; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (better(sv[w], si[w], bv, bi)) { bv = sv[w]; bi = si[w]; }
+    if (bi == 0x7fffffff) bi = 0;          // all-NaN row: numpy returns 0
+    cur[tok] = bi;
+    const int step = *d_step;
+    if (toks && step < steps) toks[(long long)tok * steps + step] = bi;
+  }
+}
+
 // NB n-blocks of 8 token rows; KW fragments per warp (K = 16 * 8 * KW);
 // NV float4 per lane per LayerNorm row (h <= 128 * NV)
 template <typename T, int NB, int KW, bool LN, int NV>
@@ -185,6 +265,10 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
 #pragma unroll
     for (int i = 0; i < 4; ++i) red[(warp * NB * 4 + nb * 4 + i) * 32 + lane] = acc[nb][i];
   __syncthreads();
+  if (a.e.mode == EPI_ARGMAX) {
+    argmax_tail(a, red, NB);
+    return;
+  }
   if (threadIdx.x < NB * 128) {
     const int e = threadIdx.x;
     float v = 0.f;
@@ -285,13 +369,22 @@ bool gemv_packed(int dtype, const void* wsrc, int M, int N, int K, const void* X
   const int rtiles = (N + 15) / 16;
   ProfScope ps(K_GEMV, st, (double)rtiles * 16 * K * 2 + (double)M * K * (ln ? 4 : 2) + (double)M * N * 4,
                2.0 * M * N * K);
+  bool ok2;
   if (dtype == EET_BF16) {
     gm::Args<__nv_bfloat16> a{w, K / 16, N, M, reinterpret_cast<const __nv_bfloat16*>(X), ldx,
                               x, x_sb, x_ss, rinfo, g, b, e};
-    return M <= 8 ? gm::dispatch<__nv_bfloat16, 1>(a, rtiles, ln, st) : gm::dispatch<__nv_bfloat16, 2>(a, rtiles, ln, st);
+    ok2 = M <= 8 ? gm::dispatch<__nv_bfloat16, 1>(a, rtiles, ln, st) : gm::dispatch<__nv_bfloat16, 2>(a, rtiles, ln, st);
+  } else {
+    gm::Args<__half> a{w, K / 16, N, M, reinterpret_cast<const __half*>(X), ldx, x, x_sb, x_ss, rinfo, g, b, e};
+    ok2 = M <= 8 ? gm::dispatch<__half, 1>(a, rtiles, ln, st) : gm::dispatch<__half, 2>(a, rtiles, ln, st);
   }
-  gm::Args<__half> a{w, K / 16, N, M, reinterpret_cast<const __half*>(X), ldx, x, x_sb, x_ss, rinfo, g, b, e};
-  return M <= 8 ? gm::dispatch<__half, 1>(a, rtiles, ln, st) : gm::dispatch<__half, 2>(a, rtiles, ln, st);
+  if (ok2 && e.mode == EPI_ARGMAX) {        // second stage of the fused argmax
+    ProfScope ps2(K_ARGMAX, st, 8.0 * rtiles * 16, 1.0 * rtiles * M);
+    launch_ex(gm::argmax_cand_kernel, dim3(M), dim3(256), 0, st, true, dim3(1, 1, 1), e.cand, rtiles, e.cur,
+              e.toks, e.steps, e.d_step);
+    EET_LAUNCH_CHECK();
+  }
+  return ok2;
 }
 
 }  // namespace eet

@@ -481,6 +481,9 @@ struct eet_runtime {
   int* h_prompts = nullptr;           // pinned staging: prompts in, tokens out
   long long* h_tokens = nullptr;
   MkState* mk = nullptr;              // decode megakernel state (packed weights, scratch)
+  int2* cand = nullptr;               // fused LM-head argmax candidates
+  int* cand_ticket = nullptr;
+  int cand_cap = 0;
 
   void* dev(size_t bytes) {
     void* p = nullptr;
@@ -859,8 +862,29 @@ static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long 
   e.ldo = m->vocab;
   // rows (b, slot): the decode plan's row map (b, 0) over x shifted by `slot`
   const float* xs = x + (long long)slot * h;
+  // packed head: argmax fused into the GEMV (no logits round trip)
+  const int rtiles = (m->vocab + 15) / 16;
+  if (rt->cand_cap < rtiles) {
+    rt->cand = (int2*)rt->dev(sizeof(int2) * (size_t)rtiles * 16);
+    rt->cand_ticket = (int*)rt->dev(sizeof(int));
+    EET_CHECK_CUDA(cudaMemsetAsync(rt->cand_ticket, 0, sizeof(int), st));
+    rt->cand_cap = rtiles;
+  }
+  Epi ea;
+  ea.mode = EPI_ARGMAX;
+  ea.out = d_logits;
+  ea.ldo = m->vocab;
+  ea.cand = rt->cand;
+  ea.ticket = rt->cand_ticket;
+  ea.cur = rt->d_cur;
+  ea.toks = d_tokens;
+  ea.d_step = rt->d_step;
+  ea.steps = steps;
+  ea.batch = batch;
   if (gemv_packed(dt, m->head, batch, m->vocab, h, nullptr, 0, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g,
-                  m->lnf_b, e, st)) {
+                  m->lnf_b, ea, st)) {
+    lg.release();
+    return;
   } else if (!(batch <= 32 && gemv_tc_ln_sm100(dt, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g, m->lnf_b,
                                                m->head, h, batch, m->vocab, h, e, st))) {
     Claim ln(rt->pool, (size_t)batch * h * es, EET_SCOPE_ACROSS, "output.layernorm");
