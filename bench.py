@@ -103,7 +103,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -123,10 +123,22 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def mark(self):
+        """index of the next sample (region bookkeeping)"""
+        return len(self.lines)
+
+    def summary(self, lo=0, hi=None):
+        """samples [lo, hi) (the timed region); falls back to the samples
+        adjacent to the region when it was shorter than the sampling period"""
+        hi = len(self.lines) if hi is None else hi
+        if hi <= lo:
+            lo, hi = max(0, lo - 1), min(len(self.lines), lo + 1)
+        return self._summary(self.lines[lo:hi])
+
+    def _summary(self, lines):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -276,6 +288,11 @@ def main():
 
     kind = w.get("kind", "generate")
     hbm, tflops, peak_src = peaks()
+    if w["dtype"] == "fp32":
+        # fp32 mode runs true-FP32 FFMA on the CUDA cores (no TF32, SURVEY
+        # App. B.4): its roofline is the FP32 SIMT peak, 148 SMs x 128 FMA/clk
+        # x 2 x 1.965 GHz (nominal; not in MEASURED_PEAKS.json)
+        tflops, peak_src = 2 * 148 * 128 * 1.965e9 / 1e12, "nominal FP32 SIMT (148 SM x 128 FMA/clk x 1.965 GHz)"
     if kind == "generate":
         cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=w["layers"],
                               head_count=w["heads"], max_prompt=w["prompt"], max_sequence=w["max_seq"],
@@ -314,6 +331,7 @@ def main():
                 return xd.to("cpu")
             return eet.decoder_layer_forward(x_dev, lw, kv, desc, eet.Phase.PROMPT_PARALLEL, pool, acts, 0)
 
+    clk = ClockSampler(torch.cuda.current_device()).__enter__()   # running before the warm-up
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -321,13 +339,15 @@ def main():
         dist.barrier()
     launches0 = _lib.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        torch.cuda.synchronize()
-        ev0.record()
-        for _ in range(args.steps):
-            step()
-        ev1.record()
-        torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    clk_lo = clk.mark()
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    clk_hi = clk.mark()
+    clk.__exit__(None, None, None)
     launches = _lib.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
     if ws > 1:
@@ -392,13 +412,27 @@ def main():
                     "timing": "profiled replay of one step: CUDA events around every launch on its "
                               "stream (event-record nodes inside the decode graph)"}
 
+    # whole-generate HBM roofline (c2): every decode step must stream all
+    # weights once (+ LM head) and every cached K/V row of the batch once
+    step_roofline = None
+    if kind == "generate":
+        h_, L_, V_, es_ = w["hidden"], w["layers"], w["vocab"], 2
+        wbytes = (12 * h_ * h_ * L_ + V_ * h_) * es_
+        kv = sum(w["batch"] * 2 * h_ * es_ * L_ * (w["prompt"] + s + 1) for s in range(w["steps"]))
+        byts = w["steps"] * wbytes + kv
+        ach = byts / (ms / args.steps / 1e3) / 1e9
+        step_roofline = {"bound": "hbm", "algorithmic_bytes_per_generate": byts, "achieved": round(ach, 1),
+                         "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+                         "note": "decode steps' weight + KV bytes over the device time of the whole generate "
+                                 "(prompt pass included in the time)"}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         v, sample = cpu_generate_sample(w) if kind == "generate" else cpu_layer_sample(w)
         cpu = {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port", "sample": sample}
 
     if rank == 0:
-        clocks = clk.summary()
+        clocks = clk.summary(clk_lo, clk_hi)
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -416,6 +450,8 @@ def main():
             "cpu_baseline": cpu,
             "kernels": kernels,
         }
+        if step_roofline:
+            line["generate_roofline"] = step_roofline
         line.update(extra)
         print(json.dumps(line), flush=True)
     if ws > 1:

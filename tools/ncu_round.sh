@@ -17,7 +17,8 @@ for w in c3 c4 c5; do
 done
 
 # full captures of the top kernels (skip the warm-up call's launches)
-timeout 600 $NCU $FULL -k regex:gemv_tc -s 400 -c 4 -o $O/gemv_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_c2.log 2>&1
+timeout 600 $NCU $FULL -k regex:gemv_mma -s 300 -c 4 -o $O/gemv_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_c2.log 2>&1
+timeout 600 $NCU $FULL -k regex:gemv_tc -s 100 -c 1 -o $O/gemv_tc_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_tc_c2.log 2>&1
 timeout 600 $NCU $FULL -k regex:attn_decode -s 60 -c 2 -o $O/attn_decode_c2 -f python tools/decode_profile.py --steps 4 > $O/attn_decode_c2.log 2>&1
 timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c3 -f python tools/layer_profile.py --workload c3 > $O/attn_tc_c3.log 2>&1
 timeout 600 $NCU $FULL -k regex:gemm_tc -s 4 -c 4 -o $O/gemm_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/gemm_tc_c4.log 2>&1
