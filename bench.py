@@ -58,7 +58,7 @@ WORKLOADS = {
     "c4": dict(hidden=4096, layers=1, heads=32, batch=8, prompt=4096, dtype="bf16", kind="layer",
                lengths="full", desc="decoder layer h4096 32 heads s4096 b8 context phase, bf16"),
     "c5": dict(hidden=12288, layers=1, heads=96, batch=1, prompt=2048, dtype="bf16", kind="layer",
-               lengths="full", desc="decoder layer h12288 96 heads s2048 b1, bf16"),
+               lengths="full", tp_ok=True, desc="decoder layer h12288 96 heads s2048 b1, bf16"),
 }
 
 HBM_KINDS = {"attn_decode", "gemv", "layernorm", "embed", "argmax", "softmax", "advance", "decode_step"}
@@ -269,6 +269,9 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--tp", type=int, default=0,
+                    help="tensor-parallel layer over the ranks (default: on for c5 under torchrun); "
+                         "--tp 1 runs the sharded path on one GPU")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload])
     if args.batch:
@@ -307,6 +310,38 @@ def main():
 
         def step(graph=True):
             return eet.generate(weights, req, cfg, pool=pool, use_graph=graph)
+    elif args.tp or (w.get("tp_ok") and ws > 1):
+        # Megatron tensor parallelism: every rank holds
+        # heads/tp heads and 4h/tp FFN columns; two NCCL all-reduces per
+        # layer. Strong scaling: all ranks process the same tokens.
+        from paper_2104_12470_b200.tp import TensorParallelLayer, shard_config
+        tp = ws if ws > 1 else 1
+        lens = lengths_for(w)
+        desc = eet.make_batch(lens)
+        s = desc.seq_len
+        cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=1,
+                              head_count=w["heads"], max_prompt=s, max_sequence=s,
+                              datatype_label=w["dtype"])
+        lw = eet.random_weights(eet.ModelConfig(1, w["hidden"], 1, w["heads"], 1, 1), 8, seed=0).layers[0]
+        pool = eet.BufferPool()
+        noop = (lambda t: None) if tp == 1 else None
+        layer = TensorParallelLayer(lw, cfg, rank, tp, pool, all_reduce=noop)
+        kv, _ = eet.preallocate_caches(shard_config(cfg, tp))
+        x_host = np.random.default_rng(1).normal(0, 1, size=(w["batch"], s, w["hidden"])).astype(np.float32)
+        x_dev = torch.from_numpy(x_host).cuda()
+        x_pin = torch.from_numpy(x_host).pin_memory()
+        units = sum(lens)
+        h2d = d2h = x_host.nbytes
+        w["desc"] = w["desc"] + f", tensor-parallel tp{tp}"
+        w["tp"] = tp
+
+        def step(graph=True, host=False):
+            kv._filled = 0
+            if host:
+                xd = x_pin.to("cuda", non_blocking=True)
+                layer.forward(xd, kv, desc, _lib.PHASE_PROMPT, 0)
+                return xd.to("cpu")
+            return layer.forward(x_dev, kv, desc, _lib.PHASE_PROMPT, 0)
     else:
         lens = lengths_for(w)
         desc = eet.make_batch(lens)
@@ -355,7 +390,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    value = ws * units * args.steps / (ms / 1e3)
+    tp_mode = bool(w.get("tp"))
+    value = (1 if tp_mode else ws) * units * args.steps / (ms / 1e3)
 
     # end to end through the public API: host inputs in, host results out
     t0 = time.perf_counter()
@@ -367,7 +403,7 @@ def main():
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = ws * units * args.steps / e2e_s
+    e2e = (1 if tp_mode else ws) * units * args.steps / e2e_s
 
     extra = {}
     if kind == "generate" and rank == 0:
@@ -436,11 +472,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if tp_mode else "weak", "vs_baseline": None,
             "dtype": {"fp16": "f16", "bf16": "bf16", "fp32": "f32"}[w["dtype"]],
             "data": "synthetic (seeded random weights N(0,0.02), random token ids / hidden states)",
             "config": {"workload": w["desc"], "batch_per_gpu": w["batch"],
-                       "parallelism": f"dp{ws}" if ws > 1 else "single",
+                       "parallelism": f"tp{w['tp']}" if tp_mode else (f"dp{ws}" if ws > 1 else "single"),
                        "l2": "working set (weights+KV) > 126 MB L2 every step; no flush needed",
                        "tokens_per_step": units},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
