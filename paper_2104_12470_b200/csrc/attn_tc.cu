@@ -20,11 +20,14 @@
 // one tile while the softmax warps of the other run.
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 namespace eet {
 namespace fa {
 using namespace sm100;
 
 constexpr int BQ = 128, BKV = 64, NSM = 8, THREADS = (NSM + 2) * 32;
+constexpr int NST = 3;                     // K/V ring stages
 constexpr float RESCALE_LOG2 = 8.0f;       // lazy rescale threshold (log2 units)
 
 template <int HD> struct Cfg {
@@ -34,7 +37,7 @@ template <int HD> struct Cfg {
   static constexpr int Q_BYTES = KSUB * QSUB;           // one query tile
   static constexpr int KV_BYTES = KSUB * KVSUB;         // one K (or V) tile
   static constexpr int P_BYTES = BQ * BKV * 2;          // 128 queries x 64 keys, one atom wide
-  static constexpr int SMEM = 2 * Q_BYTES + 4 * KV_BYTES + 2 * P_BYTES + 1024 + 256;
+  static constexpr int SMEM = 2 * Q_BYTES + 2 * NST * KV_BYTES + 2 * P_BYTES + 1024 + 256;
   // TMEM columns: S_A | S_B | O_A | O_B
   static constexpr uint32_t S_COL = 0, O_COL = 2 * BKV;
 };
@@ -49,6 +52,24 @@ __device__ __forceinline__ uint64_t smem_desc_mn(uint32_t saddr, uint32_t lbo) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
+}
+
+// exp2 on the MUFU pipe (16 / clk / SM)
+__device__ __forceinline__ float ex2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// exp2 on the FMA/ALU pipes: 2^round(x) by exponent add, 2^f (|f| <= 0.5) by
+// a cubic (max rel. error 7.7e-5, below half an fp16 ulp of P). Used for half
+// of the keys of full tiles so MUFU and FMA share the softmax (the MUFU alone
+// caps the tensor pipe near 50% at head_dim 128).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;                     // 1.5 * 2^23: round to integer
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.0550886838f, f, 0.242604051f), f, 0.693276242f), f, 0.99992894f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
 }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf) {
@@ -79,6 +100,7 @@ struct FaArgs {
   void* o; int ldo;
   int batch, seq, heads, smax, causal;
   float scale_log2;         // (1/sqrt(hd)) * log2(e)
+  int poly;                 // polynomial exp2 for half of the keys of full tiles
 };
 
 template <typename T, int HD>
@@ -104,24 +126,26 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   uint8_t* sQ = sm;                                       // [2] query tiles
-  uint8_t* sK = sQ + 2 * C::Q_BYTES;                      // [2] stages
-  uint8_t* sV = sK + 2 * C::KV_BYTES;                     // [2] stages
-  uint8_t* sP = sV + 2 * C::KV_BYTES;                     // [2] tiles
+  uint8_t* sK = sQ + 2 * C::Q_BYTES;                      // [NST] stages
+  uint8_t* sV = sK + NST * C::KV_BYTES;                   // [NST] stages
+  uint8_t* sP = sV + NST * C::KV_BYTES;                   // [2] tiles
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;      // [2]
-  uint64_t* kv_empty = bars + 3;     // [2]
-  uint64_t* s_full = bars + 5;       // [2] per tile
-  uint64_t* p_full = bars + 7;       // [2]
-  uint64_t* o_done = bars + 9;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* kv_full = bars + 1;              // [NST]
+  uint64_t* kv_empty = bars + 1 + NST;       // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;     // [2] per tile
+  uint64_t* p_full = s_full + 2;             // [2]
+  uint64_t* o_done = p_full + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&o_done[i], 1);
@@ -147,8 +171,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_2d(sQ + t * C::Q_BYTES + s * C::QSUB, &mapQ, q_full, head * HD + 64 * s,
                       a.q_rowbase[b] + q0 + t * BQ, pol);
       for (int j = 0; j < nt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        const int st = j % NST;
+        mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
         mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
         const int row = kv_row0 + pad + j * BKV;
         for (int s = 0; s < C::KSUB; ++s) {
@@ -163,36 +187,58 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t id_s = instr_desc(fmt, BQ, BKV);
       constexpr uint32_t id_o = instr_desc(fmt, BQ, HD) | (1u << 16);   // B (V) MN-major
       mbar_wait(q_full, 0);
-      for (int j = 0; j < nt; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+      // Ping-pong: while the softmax warps of one query tile work on S(j),
+      // the tensor core runs the other tile's PV(j) and S(j+1); S_t(j+1) is
+      // issued as soon as tile t's softmax has released S_t(j).
+      auto issue_s = [&](int t, int j) {
+        const uint32_t k_base = smem_u32(sK + (j % NST) * C::KV_BYTES);
+        const uint32_t q_base = smem_u32(sQ + t * C::Q_BYTES);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t qoff = (k >> 2) * C::QSUB + (k & 3) * 32;
+          const uint32_t koff = (k >> 2) * C::KVSUB + (k & 3) * 32;
+          mma_f16(tmem + C::S_COL + t * BKV, smem_desc(q_base + qoff), smem_desc(k_base + koff), id_s,
+                  k > 0);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto issue_o = [&](int t, int j) {
+        mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
-        const uint32_t k_base = smem_u32(sK + st * C::KV_BYTES);
-        const uint32_t v_base = smem_u32(sV + st * C::KV_BYTES);
-        for (int t = 0; t < 2; ++t) {                     // S_t = Q_t K_j^T
-          if (t == 0 && j >= ntA) continue;
-          const uint32_t q_base = smem_u32(sQ + t * C::Q_BYTES);
+        const uint32_t p_base = smem_u32(sP + t * C::P_BYTES);
+        const uint32_t v_base = smem_u32(sV + (j % NST) * C::KV_BYTES);
 #pragma unroll
-          for (int k = 0; k < HD / 16; ++k) {
-            const uint32_t qoff = (k >> 2) * C::QSUB + (k & 3) * 32;
-            const uint32_t koff = (k >> 2) * C::KVSUB + (k & 3) * 32;
-            mma_f16(tmem + C::S_COL + t * BKV, smem_desc(q_base + qoff), smem_desc(k_base + koff),
-                    id_s, k > 0);
+        for (int k = 0; k < BKV / 16; ++k)
+          mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
+                  smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
+        mma_commit(&o_done[t]);
+      };
+      int kv_seen = -1;
+      auto wait_kv = [&](int j) {
+        if (kv_seen >= j) return;
+        mbar_wait(&kv_full[j % NST], (j / NST) & 1);
+        tc_fence_after();
+        kv_seen = j;
+      };
+      if (nt > 0) {
+        wait_kv(0);
+        if (ntA > 0) issue_s(0, 0);
+        issue_s(1, 0);
+      }
+      for (int j = 0; j < nt; ++j) {
+        if (j < ntA) {
+          issue_o(0, j);
+          if (j + 1 < ntA) {
+            wait_kv(j + 1);
+            issue_s(0, j + 1);
           }
-          mma_commit(&s_full[t]);
         }
-        for (int t = 0; t < 2; ++t) {                     // O_t += P_t V_j
-          if (t == 0 && j >= ntA) continue;
-          mbar_wait(&p_full[t], j & 1);
-          tc_fence_after();
-          const uint32_t p_base = smem_u32(sP + t * C::P_BYTES);
-#pragma unroll
-          for (int k = 0; k < BKV / 16; ++k)
-            mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
-                    smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
-          mma_commit(&o_done[t]);
+        issue_o(1, j);
+        if (j + 1 < nt) {
+          wait_kv(j + 1);
+          issue_s(1, j + 1);
         }
-        mma_commit(&kv_empty[st]);
+        mma_commit(&kv_empty[j % NST]);
       }
     }
   } else {
@@ -224,12 +270,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[32 + i] = __uint_as_float(r[i]);
       }
+      // raw scores; masking only on tiles that cut a causal / pad bound
+      const bool full = __all_sync(0xffffffffu, nvalid == BKV);
       float tmax = -INFINITY;
+      if (full) {
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) {
-        sv[i] = (i < nvalid) ? sv[i] * a.scale_log2 : -INFINITY;
-        tmax = fmaxf(tmax, sv[i]);
+        for (int i = 0; i < BKV; ++i) tmax = fmaxf(tmax, sv[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < BKV; ++i) {
+          sv[i] = (i < nvalid) ? sv[i] : -INFINITY;
+          tmax = fmaxf(tmax, sv[i]);
+        }
       }
+      tmax *= a.scale_log2;                               // scale > 0: max commutes
       // O rows and P buffer of tile j-1 must be done before we touch them
       if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);
       tc_fence_after();
@@ -254,14 +308,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         m = tmax;                                         // first live tile of this row
       }
       const float msub = (m == -INFINITY) ? 0.f : m;
+      const float sc = a.scale_log2;
       float rs = 0.f;
+      // p = 2^(s * scale_log2 - m): one FFMA + exp2 per key; on full tiles
+      // every other 8-key chunk takes the polynomial exp2
 #pragma unroll
       for (int c = 0; c < BKV / 8; ++c) {                 // 8 keys -> one 16 B swizzled chunk
         uint32_t pk[4];
+        const bool poly = a.poly && full && (c & 1);
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
-          const float p0 = exp2f(sv[c * 8 + i] - msub);
-          const float p1 = exp2f(sv[c * 8 + i + 1] - msub);
+          const float x0 = fmaf(sv[c * 8 + i], sc, -msub), x1 = fmaf(sv[c * 8 + i + 1], sc, -msub);
+          const float p0 = poly ? ex2_poly(x0) : ex2_mufu(x0);
+          const float p1 = poly ? ex2_poly(x1) : ex2_mufu(x1);
           rs += p0 + p1;
           pk[i >> 1] = pack2(p0, p1, BF);
         }
@@ -319,6 +378,11 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   a.smax = (int)(p.k_sh / p.hd);
   a.causal = p.causal;
   a.scale_log2 = p.scale * 1.4426950408889634f;
+  static const int poly = [] {            // opt-in: measured slower at c3/c4 (r01)
+    const char* e = std::getenv("EET_ATTN_POLY");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  a.poly = poly;
   auto kern = attn_tc_kernel<T, HD>;
   static bool attr = false;
   if (!attr) {
