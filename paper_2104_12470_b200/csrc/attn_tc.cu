@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int c = 0; c < BKV / 8; ++c) {                 // 8 keys -> one 16 B swizzled chunk
         uint32_t pk[4];
-        const bool poly = a.poly && full && (c & 1);
+        const bool poly = a.poly && full && ((a.poly == 1) ? (c & 1) : ((c & 3) == 3));
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
           const float x0 = fmaf(sv[c * 8 + i], sc, -msub), x1 = fmaf(sv[c * 8 + i + 1], sc, -msub);
@@ -380,7 +380,7 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   a.scale_log2 = p.scale * 1.4426950408889634f;
   static const int poly = [] {            // opt-in: measured slower at c3/c4 (r01)
     const char* e = std::getenv("EET_ATTN_POLY");
-    return (e && e[0] == '1') ? 1 : 0;
+    return e ? atoi(e) : 0;          // 1: half of the chunks, 2: a quarter
   }();
   a.poly = poly;
   auto kern = attn_tc_kernel<T, HD>;

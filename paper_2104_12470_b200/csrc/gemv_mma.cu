@@ -141,18 +141,21 @@ __global__ void __launch_bounds__(256) argmax_cand_kernel(const int2* __restrict
 
 // NB n-blocks of 8 token rows; KW fragments per warp (K = 16 * 8 * KW);
 // NV float4 per lane per LayerNorm row (h <= 128 * NV)
-template <typename T, int NB, int KW, bool LN, int NV>
+// SPLIT = 2: a 2-CTA cluster shares one tile, each CTA half of K, and the
+// halves are summed through distributed shared memory (rank 0 + rank 1).
+template <typename T, int NB, int KW, bool LN, int NV, int SPLIT>
 __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant__ Args<T> a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int K = a.ks * 16, xst = K + XPAD;
+  const int K = a.ks * 16 / SPLIT, xst = K + XPAD;                      // K: this CTA's span
   T* xs = reinterpret_cast<T*>(smem);                                   // [16][K + XPAD]
   float* red = reinterpret_cast<float*>(smem + (size_t)16 * xst * sizeof(T));   // [WARPS][NB*4][32]
-  const int rt = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rt = blockIdx.x / SPLIT, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = SPLIT == 2 ? (int)sm100::cluster_ctarank() : 0;
 
   // 1. this warp's weight slice -> registers (static data: before the wait)
   uint4 wv[KW];
   {
-    const uint4* wp = a.w + ((size_t)rt * a.ks + (size_t)warp * KW) * 32 + lane;
+    const uint4* wp = a.w + ((size_t)rt * a.ks + (size_t)half * (a.ks / SPLIT) + (size_t)warp * KW) * 32 + lane;
 #pragma unroll
     for (int i = 0; i < KW; ++i) wv[i] = ldg_stream(wp + i * 32);
   }
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
       for (int u = 0; u < 4; ++u) {
         const int i = base + u * THREADS + threadIdx.x;
         const int r = i / w8, c = i - r * w8;
-        v[u] = (i < 16 * w8 && r < a.M) ? reinterpret_cast<const uint4*>(a.X + (size_t)r * a.ldx)[c]
+        v[u] = (i < 16 * w8 && r < a.M) ? reinterpret_cast<const uint4*>(a.X + (size_t)r * a.ldx + half * K)[c]
                                         : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
@@ -269,11 +272,21 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
     argmax_tail(a, red, NB);
     return;
   }
+  float v = 0.f;
+  if (threadIdx.x < NB * 128) {
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) v += red[(w * NB * 4) * 32 + threadIdx.x];
+  }
+  if constexpr (SPLIT == 2) {
+    float* part = red + WARPS * NB * 4 * 32;                              // [NB*128]
+    if (half == 1 && threadIdx.x < NB * 128) part[threadIdx.x] = v;
+    sm100::cluster_sync();
+    if (half == 0 && threadIdx.x < NB * 128) v += sm100::map_peer(part, 1)[threadIdx.x];
+    sm100::cluster_sync();                                                // peer smem stays live
+    if (half == 1) return;
+  }
   if (threadIdx.x < NB * 128) {
     const int e = threadIdx.x;
-    float v = 0.f;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) v += red[(w * NB * 4) * 32 + e];
     const int i = e >> 5, ln = e & 31;
     const int row = (ln >> 2) + 8 * ((i & 3) >> 1);
     const int tok = (i >> 2) * 8 + 2 * (ln & 3) + (i & 1);
@@ -282,17 +295,17 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
   }
 }
 
-template <typename T, int NB, int KW, bool LN, int NV>
+template <typename T, int NB, int KW, bool LN, int NV, int SPLIT = 1>
 static void go(const Args<T>& a, int rtiles, cudaStream_t st) {
-  auto kern = gemv_mma_kernel<T, NB, KW, LN, NV>;
-  const size_t smem = (size_t)16 * (a.ks * 16 + XPAD) * sizeof(T) + (size_t)WARPS * NB * 4 * 32 * 4 +
-                      (LN ? (size_t)2 * a.ks * 16 * 4 : 0);
+  auto kern = gemv_mma_kernel<T, NB, KW, LN, NV, SPLIT>;
+  const size_t smem = (size_t)16 * (a.ks * 16 / SPLIT + XPAD) * sizeof(T) + (size_t)WARPS * NB * 4 * 32 * 4 +
+                      (LN ? (size_t)2 * a.ks * 16 * 4 : 0) + (SPLIT == 2 ? (size_t)NB * 128 * 4 : 0);
   static size_t set = 0;
   if (set < smem) {
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = smem;
   }
-  launch_ex(kern, dim3(rtiles), dim3(THREADS), smem, st, true, dim3(1, 1, 1), a);
+  launch_ex(kern, dim3(rtiles * SPLIT), dim3(THREADS), smem, st, true, dim3(SPLIT, 1, 1), a);
   EET_LAUNCH_CHECK();
 }
 
@@ -313,7 +326,7 @@ static bool dispatch(const Args<T>& a, int rtiles, bool ln, cudaStream_t st) {
     case 1024: go<T, NB, 8, false, 1>(a, rtiles, st); return true;
     case 2048: go<T, NB, 16, false, 1>(a, rtiles, st); return true;
     case 3072: go<T, NB, 24, false, 1>(a, rtiles, st); return true;
-    case 4096: go<T, NB, 32, false, 1>(a, rtiles, st); return true;
+    case 4096: go<T, NB, 16, false, 1, 2>(a, rtiles, st); return true;      // 2-CTA K split
     default: return false;
   }
 }
@@ -359,9 +372,9 @@ bool gemv_packed(int dtype, const void* wsrc, int M, int N, int K, const void* X
               reinterpret_cast<uintptr_t>(b)) & 15 || (x_sb & 3) || (x_ss & 3)))
     return false;
   if (!ln && ((reinterpret_cast<uintptr_t>(X) & 15) || (ldx % 8))) return false;
-  // K > 1024 (W2) stays on the tcgen05 split-K kernel: one CTA per 16-row
-  // tile cannot keep enough bytes in flight there (graph bench r01: 7.2 vs
-  // 5.2 us at 1024 x 4096)
+  // K > 1024 (W2) stays on the tcgen05 split-K kernel: in the decode graph
+  // it costs 6.7 us per layer vs 7.2 us for the 2-CTA-cluster packed variant
+  // (SPLIT = 2 below) and ~7.2 us for one CTA per tile (r01 A/B)
   const int kl[] = {256, 512, 768, 1024}, kp[] = {256, 512, 768, 1024};
   bool ok = false;
   if (ln) { for (int k : kl) ok |= K == k; } else { for (int k : kp) ok |= K == k; }

@@ -1,6 +1,4 @@
 for i in 1 2; do
-for v in 0 1; do EET_ATTN_NOPOLY=$v timeout 300 python bench.py --workload c4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b.json 2>/dev/null; python -c "
-import json; d=json.load(open('gpurun_out/b.json')); print('nopoly=$v c4', round(d['ms_per_step'],3), {k:(v['ms'],v['frac']) for k,v in d['kernels'].items()})"; done
-for v in 0 1; do EET_ATTN_NOPOLY=$v timeout 300 python bench.py --workload c3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b.json 2>/dev/null; python -c "
-import json; d=json.load(open('gpurun_out/b.json')); print('nopoly=$v c3', round(d['ms_per_step'],3), {k:(v['ms'],v['frac']) for k,v in d['kernels'].items()})"; done
+for v in 0 1 2; do EET_ATTN_POLY=$v timeout 300 python bench.py --workload c4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/b.json')); print('poly=$v c4', round(d['ms_per_step'],3), {k:(v['ms'],v['frac']) for k,v in d['kernels'].items() if k=='attn_prefill'})"; done
 done
