@@ -868,9 +868,22 @@ static void decode_launch(const DecodeArgs& a, cudaStream_t st) {
   EET_LAUNCH_CHECK();
 }
 
+template <typename T, int E, int LPK, int NBUF>
+static void decode_bulk_launch_n(const DecodeArgs& a, cudaStream_t st);
+
 template <typename T, int E, int LPK>
 static void decode_bulk_launch(const DecodeArgs& a, cudaStream_t st) {
-  constexpr int NBUF = (E * LPK * sizeof(T) <= 128) ? 4 : 2;   // ring <= 64 KB
+  constexpr int NB0 = (E * LPK * sizeof(T) <= 128) ? 4 : 2;    // ring <= 64 KB
+  static const int deep = [] {                                  // A/B: 6-chunk ring
+    const char* e = std::getenv("EET_ATTN_NBUF6");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  if (NB0 == 4 && deep) return decode_bulk_launch_n<T, E, LPK, 6>(a, st);
+  return decode_bulk_launch_n<T, E, LPK, NB0>(a, st);
+}
+
+template <typename T, int E, int LPK, int NBUF>
+static void decode_bulk_launch_n(const DecodeArgs& a, cudaStream_t st) {
   dim3 grid(a.splits, a.heads, a.batch);
   double keys = 0;
   for (int b = 0; b < a.batch; ++b)

@@ -37,9 +37,11 @@ template <int HD> struct Cfg {
   static constexpr int Q_BYTES = KSUB * QSUB;           // one query tile
   static constexpr int KV_BYTES = KSUB * KVSUB;         // one K (or V) tile
   static constexpr int P_BYTES = BQ * BKV * 2;          // 128 queries x 64 keys, one atom wide
-  static constexpr int SMEM = 2 * Q_BYTES + 2 * NST * KV_BYTES + 2 * P_BYTES + 1024 + 256;
+  // P double-buffered per tile: softmax(j+1) writes while PV(j) reads
+  static constexpr int SMEM = 2 * Q_BYTES + 2 * NST * KV_BYTES + 4 * P_BYTES + 1024 + 256;
   // TMEM columns: S_A | S_B | O_A | O_B
-  static constexpr uint32_t S_COL = 0, O_COL = 2 * BKV;
+  // TMEM columns: S_A[2] | S_B[2] (double-buffered scores) | O_A | O_B
+  static constexpr uint32_t S_COL = 0, O_COL = 4 * BKV;
 };
 
 // V is read MN-major: 8-key row groups 1024 B apart (SBO), 64-wide hd blocks
@@ -70,6 +72,50 @@ __device__ __forceinline__ float ex2_poly(float x) {
   const float f = x - (t - 12582912.f);
   const float p = fmaf(fmaf(fmaf(0.0550886838f, f, 0.242604051f), f, 0.693276242f), f, 0.99992894f);
   return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
+// packed f32x2 math (FFMA2 / FADD2) for the softmax of full tiles
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (cubic on |f| <= 0.5, exponent by IMAD)
+__device__ __forceinline__ uint64_t ex2_poly2(uint64_t x2) {
+  float a, b;
+  f2unpack(x2, a, b);
+  x2 = f2pack(fmaxf(a, -126.f), fmaxf(b, -126.f));
+  const uint64_t magic = f2pack(12582912.f, 12582912.f), nmagic = f2pack(-12582912.f, -12582912.f);
+  const uint64_t t = fadd2(x2, magic);                       // round to integer (low mantissa bits)
+  const uint64_t r = fadd2(t, nmagic);
+  const uint64_t f = ffma2(r, f2pack(-1.f, -1.f), x2);       // x - round(x)
+  uint64_t p = ffma2(f2pack(0.0550886838f, 0.0550886838f), f, f2pack(0.242604051f, 0.242604051f));
+  p = ffma2(p, f, f2pack(0.693276242f, 0.693276242f));
+  p = ffma2(p, f, f2pack(0.99992894f, 0.99992894f));
+  float t0, t1, p0, p1;
+  f2unpack(t, t0, t1);
+  f2unpack(p, p0, p1);
+  // (bits(t) - bits(1.5 * 2^23)) << 23 == bits(t) << 23 (mod 2^32)
+  return f2pack(__int_as_float(__float_as_int(t0) * (1 << 23) + __float_as_int(p0)),
+                __int_as_float(__float_as_int(t1) * (1 << 23) + __float_as_int(p1)));
 }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b, bool bf) {
@@ -129,14 +175,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sK = sQ + 2 * C::Q_BYTES;                      // [NST] stages
   uint8_t* sV = sK + NST * C::KV_BYTES;                   // [NST] stages
   uint8_t* sP = sV + NST * C::KV_BYTES;                   // [2] tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * C::P_BYTES);     // sP: [2 tiles][2 buffers]
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;              // [NST]
   uint64_t* kv_empty = bars + 1 + NST;       // [NST]
-  uint64_t* s_full = bars + 1 + 2 * NST;     // [2] per tile
-  uint64_t* p_full = s_full + 2;             // [2]
-  uint64_t* o_done = p_full + 2;             // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* s_full = bars + 1 + 2 * NST;     // [2 tiles][2 buffers]
+  uint64_t* p_full = s_full + 4;             // [2 tiles][2 P buffers]: P(j) in buffer j & 1
+  uint64_t* o_done = p_full + 4;             // [2 tiles][2 P buffers]: PV(j) on buffer j & 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -145,10 +191,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&o_done[i], 1);
+      mbar_init(&p_full[2 * i], 128);
+      mbar_init(&p_full[2 * i + 1], 128);
+      mbar_init(&o_done[2 * i], 1);
+      mbar_init(&o_done[2 * i + 1], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapQ) : "memory");
@@ -197,21 +245,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t qoff = (k >> 2) * C::QSUB + (k & 3) * 32;
           const uint32_t koff = (k >> 2) * C::KVSUB + (k & 3) * 32;
-          mma_f16(tmem + C::S_COL + t * BKV, smem_desc(q_base + qoff), smem_desc(k_base + koff), id_s,
-                  k > 0);
+          mma_f16(tmem + C::S_COL + (t * 2 + (j & 1)) * BKV, smem_desc(q_base + qoff),
+                  smem_desc(k_base + koff), id_s, k > 0);
         }
-        mma_commit(&s_full[t]);
+        mma_commit(&s_full[t * 2 + (j & 1)]);
       };
       auto issue_o = [&](int t, int j) {
-        mbar_wait(&p_full[t], j & 1);
+        mbar_wait(&p_full[t * 2 + (j & 1)], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t p_base = smem_u32(sP + t * C::P_BYTES);
+        const uint32_t p_base = smem_u32(sP + (t * 2 + (j & 1)) * C::P_BYTES);
         const uint32_t v_base = smem_u32(sV + (j % NST) * C::KV_BYTES);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
           mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
                   smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
-        mma_commit(&o_done[t]);
+        mma_commit(&o_done[t * 2 + (j & 1)]);
       };
       int kv_seen = -1;
       auto wait_kv = [&](int j) {
@@ -220,23 +268,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         kv_seen = j;
       };
-      if (nt > 0) {
-        wait_kv(0);
-        if (ntA > 0) issue_s(0, 0);
-        issue_s(1, 0);
+      // S is double-buffered per tile: S_t(j+2) goes out as soon as the
+      // softmax of tile t has released S_t(j) (its P(j) is in smem)
+      for (int j = 0; j < 2 && j < nt; ++j) {
+        wait_kv(j);
+        if (j < ntA) issue_s(0, j);
+        issue_s(1, j);
       }
       for (int j = 0; j < nt; ++j) {
         if (j < ntA) {
           issue_o(0, j);
-          if (j + 1 < ntA) {
-            wait_kv(j + 1);
-            issue_s(0, j + 1);
+          if (j + 2 < ntA) {
+            wait_kv(j + 2);
+            issue_s(0, j + 2);
           }
         }
         issue_o(1, j);
-        if (j + 1 < nt) {
-          wait_kv(j + 1);
-          issue_s(1, j + 1);
+        if (j + 2 < nt) {
+          wait_kv(j + 2);
+          issue_s(1, j + 2);
         }
         mma_commit(&kv_empty[j % NST]);
       }
@@ -251,14 +301,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool live = qs >= pad && qs < a.seq;
     const int row_kend = live ? (a.causal ? qs + 1 : a.seq) : pad;   // keys [pad, row_kend)
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + C::S_COL + t * BKV;
+    const uint32_t s_base = tmem + lane_addr + C::S_COL + t * 2 * BKV;
     const uint32_t o_addr = tmem + lane_addr + C::O_COL + t * HD;
-    uint8_t* prow = sP + t * C::P_BYTES + row * 128;
+    uint8_t* prow0 = sP + (t * 2) * C::P_BYTES + row * 128;
     float m = -INFINITY, l = 0.f;                         // m in log2 units (scaled)
     for (int j = 0; j < ntile; ++j) {
       const int kt = pad + j * BKV;
       const int nvalid = min(max(row_kend - kt, 0), BKV);
-      mbar_wait(&s_full[t], j & 1);
+      mbar_wait(&s_full[t * 2 + (j & 1)], (j >> 1) & 1);
+      const uint32_t s_addr = s_base + (j & 1) * BKV;
       tc_fence_after();
       float sv[BKV];
       {
@@ -275,7 +326,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       float tmax = -INFINITY;
       if (full) {
 #pragma unroll
-        for (int i = 0; i < BKV; ++i) tmax = fmaxf(tmax, sv[i]);
+        for (int i = 0; i < BKV; i += 2) tmax = fmax3(tmax, sv[i], sv[i + 1]);
       } else {
 #pragma unroll
         for (int i = 0; i < BKV; ++i) {
@@ -284,14 +335,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       tmax *= a.scale_log2;                               // scale > 0: max commutes
-      // O rows and P buffer of tile j-1 must be done before we touch them
-      if (j > 0) mbar_wait(&o_done[t], (j - 1) & 1);
+      // P buffer j & 1 was last read by PV(j-2)
+      uint8_t* prow = prow0 + (j & 1) * C::P_BYTES;
+      if (j >= 2) mbar_wait(&o_done[t * 2 + (j & 1)], ((j - 2) >> 1) & 1);
       tc_fence_after();
       // tcgen05.ld/st are .sync.aligned: the O rescale is decided per warp
       // (any row whose max grew past the threshold rescales the whole warp;
       // rescaling a row that did not need it is exact up to rounding)
       const bool need = tmax > m + RESCALE_LOG2 || (m == -INFINITY && tmax != -INFINITY);
       if (__any_sync(0xffffffffu, need && m != -INFINITY)) {
+        // the O rows must be final up to PV(j-1) before they are rescaled
+        if (j >= 1) mbar_wait(&o_done[t * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+        tc_fence_after();
         const float m_new = fmaxf(m, tmax);
         const float f = (m == -INFINITY) ? 1.f : exp2f(m - m_new);   // -inf row: O is still zero
         l *= f;
@@ -310,28 +365,57 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float msub = (m == -INFINITY) ? 0.f : m;
       const float sc = a.scale_log2;
       float rs = 0.f;
-      // p = 2^(s * scale_log2 - m): one FFMA + exp2 per key; on full tiles
-      // every other 8-key chunk takes the polynomial exp2
+      if (full) {
+        // p = 2^(s * scale_log2 - m) in f32x2 pairs; chunks 1, 4, 6 (3/8 of
+        // the keys) take the FMA-pipe polynomial, the rest the MUFU: balances
+        // the 16/clk MUFU against the issue slots (the MUFU alone caps the
+        // tensor pipe near 50% at head_dim 128)
+        const uint64_t sc2 = f2pack(sc, sc), nm2 = f2pack(-msub, -msub);
+        uint64_t rs2 = f2pack(0.f, 0.f);
 #pragma unroll
-      for (int c = 0; c < BKV / 8; ++c) {                 // 8 keys -> one 16 B swizzled chunk
-        uint32_t pk[4];
-        const bool poly = a.poly && full && ((a.poly == 1) ? (c & 1) : ((c & 3) == 3));
+        for (int c = 0; c < BKV / 8; ++c) {
+          uint32_t pk[4];
 #pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-          const float x0 = fmaf(sv[c * 8 + i], sc, -msub), x1 = fmaf(sv[c * 8 + i + 1], sc, -msub);
-          const float p0 = poly ? ex2_poly(x0) : ex2_mufu(x0);
-          const float p1 = poly ? ex2_poly(x1) : ex2_mufu(x1);
-          rs += p0 + p1;
-          pk[i >> 1] = pack2(p0, p1, BF);
+          for (int i = 0; i < 8; i += 2) {
+            const uint64_t x2 = ffma2(f2pack(sv[c * 8 + i], sv[c * 8 + i + 1]), sc2, nm2);
+            uint64_t p2;
+            if (a.poly && (c == 1 || c == 4 || c == 6)) {
+              p2 = ex2_poly2(x2);
+            } else {
+              float x0, x1;
+              f2unpack(x2, x0, x1);
+              p2 = f2pack(ex2_mufu(x0), ex2_mufu(x1));
+            }
+            rs2 = fadd2(rs2, p2);
+            float p0, p1;
+            f2unpack(p2, p0, p1);
+            pk[i >> 1] = pack2(p0, p1, BF);
+          }
+          *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
-        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        float r0, r1;
+        f2unpack(rs2, r0, r1);
+        rs = r0 + r1;
+      } else {
+#pragma unroll
+        for (int c = 0; c < BKV / 8; ++c) {                 // 8 keys -> one 16 B swizzled chunk
+          uint32_t pk[4];
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            const float p0 = ex2_mufu(fmaf(sv[c * 8 + i], sc, -msub));
+            const float p1 = ex2_mufu(fmaf(sv[c * 8 + i + 1], sc, -msub));
+            rs += p0 + p1;
+            pk[i >> 1] = pack2(p0, p1, BF);
+          }
+          *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
       }
       l += rs;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
       tc_fence_before();
-      mbar_arrive(&p_full[t]);
+      mbar_arrive(&p_full[t * 2 + (j & 1)]);
     }
-    if (ntile > 0) mbar_wait(&o_done[t], (ntile - 1) & 1);
+    if (ntile > 0) mbar_wait(&o_done[t * 2 + ((ntile - 1) & 1)], ((ntile - 1) >> 1) & 1);
     tc_fence_after();
     if (ntile > 0) {                                      // warp-uniform TMEM reads
       const float inv = l > 0.f ? 1.0f / l : 0.f;
@@ -378,9 +462,9 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   a.smax = (int)(p.k_sh / p.hd);
   a.causal = p.causal;
   a.scale_log2 = p.scale * 1.4426950408889634f;
-  static const int poly = [] {            // opt-in: measured slower at c3/c4 (r01)
+  static const int poly = [] {            // A/B switch: EET_ATTN_POLY=0 -> MUFU only
     const char* e = std::getenv("EET_ATTN_POLY");
-    return e ? atoi(e) : 0;          // 1: half of the chunks, 2: a quarter
+    return e ? atoi(e) : 1;
   }();
   a.poly = poly;
   auto kern = attn_tc_kernel<T, HD>;
