@@ -7,7 +7,9 @@
 //    weight read, so it streams W with 128-bit loads and keeps the few
 //    activation rows in shared memory. Works for every dtype.
 // Both compute C = A[M,K] * B[N,K]^T with the fused epilogue of common.cuh.
-#include "common.cuh"
+#include "sm100.cuh"
+
+#include <algorithm>
 
 namespace eet {
 
@@ -16,14 +18,22 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16;
 }
 
+// split-K: blockIdx.z = split, K range [z * kspan, (z+1) * kspan); with
+// part != nullptr the tile is stored raw to part[z][M][N] (the reduction
+// kernel applies the epilogue), else the epilogue runs here.
 __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, int lda,
                                                        const float* __restrict__ B, int ldb,
-                                                       int M, int N, int K, Epi e) {
+                                                       int M, int N, int K, Epi e, int kspan,
+                                                       float* __restrict__ part) {
   __shared__ __align__(16) float As[2][BK][BM + 4];
   __shared__ __align__(16) float Bs[2][BK][BN + 4];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kbeg = blockIdx.z * kspan;
+  A += kbeg;
+  B += kbeg;
+  K = min(kspan, K - kbeg);
   // loader mapping: 64 rows x 16 k = 1024 elements; thread -> row lr, k lk..lk+3
   const int lr = tid >> 2, lk = (tid & 3) * 4;
   float acc[4][4] = {};
@@ -73,18 +83,62 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int n = n0 + tx * 4 + j;
-      if (n < N) epi_apply<float>(e, m, n, acc[i][j]);
+      if (n >= N) continue;
+      if (part) part[((size_t)blockIdx.z * M + m) * N + n] = acc[i][j];
+      else epi_apply<float>(e, m, n, acc[i][j]);
     }
   }
 }
 
+// second stage of split-K: partial sums in split order (deterministic), epilogue
+__global__ void gemm_f32_reduce_kernel(const float* __restrict__ part, int splits, int M, int N, Epi e) {
+  const long long total = (long long)M * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int s = 0; s < splits; ++s) v += part[s * total + i];
+    epi_apply<float>(e, (int)(i / N), (int)(i % N), v);
+  }
+}
+
+// Split-K plan: ~4 CTAs of 256 threads per SM, >= 128 k per split. The
+// partial workspace is device memory grown outside graph capture; under
+// capture (or if it would have to grow) the GEMM runs unsplit.
 void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M, int N, int K,
                    const Epi& e, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  const int tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+  int splits = std::max(1, std::min(4 * device_sm_count() / std::max(1, tiles), K / 128));
+  static float* ws = nullptr;
+  static size_t ws_bytes = 0;
+  if (splits > 1) {
+    const size_t need = sizeof(float) * (size_t)splits * M * N;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (need > ws_bytes) {
+      if (cs != cudaStreamCaptureStatusNone) {
+        splits = 1;
+      } else {
+        EET_CHECK_CUDA(cudaStreamSynchronize(st));
+        if (ws) cudaFree(ws);
+        EET_CHECK_CUDA(cudaMalloc(&ws, need));
+        ws_bytes = need;
+      }
+    }
+  }
+  const int kspan = ((K + splits - 1) / splits + BK - 1) / BK * BK;
+  splits = (K + kspan - 1) / kspan;
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, splits);
   ProfScope ps(K_GEMM_F32, st, gemm_bytes(M, N, K, 4, e), 2.0 * M * N * K);
-  gemm_f32_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e);
+  gemm_f32_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, splits > 1 ? ws : nullptr);
   EET_LAUNCH_CHECK();
+  if (splits > 1) {
+    const long long total = (long long)M * N;
+    gemm_f32_reduce_kernel<<<(int)std::min<long long>((total + 255) / 256, 8 * device_sm_count()), 256, 0, st>>>(
+        ws, splits, M, N, e);
+    count_launch();
+    EET_LAUNCH_CHECK();
+  }
 }
 
 // --------------------------------------------------------- small-M GEMV

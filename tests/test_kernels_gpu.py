@@ -159,8 +159,10 @@ def _gemm(dtype_code, a, b, bias=None):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (7, 100, 40), (16, 3072, 1024), (17, 50, 24),
-                                   (205, 2304, 768), (300, 130, 100)])
+                                   (205, 2304, 768), (300, 130, 100), (205, 768, 3072), (64, 64, 4100)])
 def test_fp32_gemm_exact_path(eet, M, N, K):
+    """True-fp32 GEMM (split-K with an ordered second-stage reduction for
+    small M x N) against fp64."""
     rng = np.random.default_rng(M * 7 + N)
     a = rng.normal(size=(M, K)).astype(np.float32)
     b = rng.normal(size=(N, K)).astype(np.float32)
