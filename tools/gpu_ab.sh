@@ -1,5 +1,6 @@
 export PYTHONUNBUFFERED=1
-EET_SKIP=qkv,o,w1,w2 timeout 200 python tools/decode_step_time.py | sed "s/^/attn bulk /"
-EET_ATTN_RANGE=1 EET_SKIP=qkv,o,w1,w2 timeout 200 python tools/decode_step_time.py | sed "s/^/attn range /"
-EET_ATTN_RANGE=1 EET_ATTN_NOMERGE=1 EET_SKIP=qkv,o,w1,w2 timeout 200 python tools/decode_step_time.py | sed "s/^/attn range-nomerge /"
-EET_SKIP=qkv,attn,o,w1,w2 timeout 200 python tools/decode_step_time.py | sed "s/^/none /"
+EET_GEMV_TPC2=1 timeout 300 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "16bit or generate or megakernel" 2>&1 | tail -1
+for i in 1 2; do
+timeout 200 python tools/decode_step_time.py | sed "s/^/tpc1 /"
+EET_GEMV_TPC2=1 timeout 200 python tools/decode_step_time.py | sed "s/^/tpc2 /"
+done
