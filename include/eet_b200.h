@@ -141,6 +141,14 @@ int eet_gemm(int dtype, const void* A, const void* B, const float* bias,
 int eet_gemv_packed(int dtype, const void* w, int N, int K, const void* X, int M,
                     float* out, int repack, void* stream);
 
+/* Calibration: n dependent launches of an empty kernel (ctas CTAs), with or
+ * without programmatic dependent launch; counter may be NULL. */
+int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream);
+
+/* Development trace of the packed decode GEMV: on = 1 resets and enables,
+ * on = 0 disables and copies 4096 x 8 stamps to out (n = records). */
+int eet_debug_ktrace(int on, long long* out, int* n);
+
 /* ------------------------------------------------------------ layer path */
 typedef struct {
   const float* ln1_g; const float* ln1_b;      /* [h]                   */

@@ -24,6 +24,18 @@ namespace gm {
 
 constexpr int WARPS = 8, THREADS = WARPS * 32, XPAD = 8;
 
+// development trace (EET_KTRACE=1): CTA 0 of every launch records
+// globaltimer stamps [start, weights issued, wait passed, X staged, MMA done,
+// reduced, end] plus (N, K) into a ring
+__device__ int g_ktrace_on = 0;
+__device__ unsigned g_ktrace_n = 0;
+__device__ long long g_ktrace[4096][8];
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <typename T>
 struct Args {
   const uint4* w;                 // packed [rtiles][ks][32] uint4
@@ -93,7 +105,7 @@ __device__ __noinline__ void argmax_tail(const Args<T>& a, const float* red, int
     }
   }
   __syncthreads();
-  if (threadIdx.x < a.M) {
+  if (threadIdx.x < a.M && rt * 16 < a.N) {
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     for (int r = 0; r < 16; ++r)
@@ -143,7 +155,7 @@ __global__ void __launch_bounds__(256) argmax_cand_kernel(const int2* __restrict
 // NV float4 per lane per LayerNorm row (h <= 128 * NV)
 // SPLIT = 2: a 2-CTA cluster shares one tile, each CTA half of K, and the
 // halves are summed through distributed shared memory (rank 0 + rank 1).
-template <typename T, int NB, int KW, bool LN, int NV, int SPLIT, int TPC>
+template <typename T, int NB, int KW, bool LN, int NV, int SPLIT, int TPC, int CL = 1>
 __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant__ Args<T> a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int K = a.ks * 16 / SPLIT, xst = K + XPAD;                      // K: this CTA's span
@@ -155,6 +167,9 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
   const int half = SPLIT == 2 ? (int)sm100::cluster_ctarank() : 0;
   const int rtiles = (a.N + 15) / 16;
 
+  const bool trace = g_ktrace_on && blockIdx.x == 0 && threadIdx.x == 0;
+  long long ts[7];
+  if (trace) ts[0] = gtime();
   // 1. this warp's weight slice -> registers (static data: before the wait)
   uint4 wv[TPC][KW];
 #pragma unroll
@@ -172,8 +187,10 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
       reinterpret_cast<float4*>(sgb + K)[i] = __ldg(reinterpret_cast<const float4*>(a.b) + i);
     }
   }
+  if (trace) ts[1] = gtime();
   sm100::griddep_wait();
   sm100::griddep_launch_dependents();
+  if (trace) ts[2] = gtime();
 
   // 2. activation rows -> xs (rows >= M are zero)
   if constexpr (LN) {
@@ -247,6 +264,7 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
     }
   }
   __syncthreads();
+  if (trace) ts[3] = gtime();
 
   // 3. this warp's K slice on the tensor cores
   float acc[TPC][NB][4];
@@ -269,6 +287,10 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
         for (int u = 0; u < TPC; ++u) mma16816<T>(acc[u][nb], wv[u][i], b0, b1);
       }
     }
+  }
+  if (trace) {
+    float z = acc[0][0][0];                     // MMA results materialised
+    if (z == 1.2345e-38f) ts[4] = 0; else ts[4] = gtime();
   }
   // 4. warp-ordered reduction + epilogue
 #pragma unroll
@@ -303,6 +325,7 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) v += red[(w * NB * 4) * 32 + threadIdx.x];
   }
+  if (trace) ts[5] = gtime();
   if constexpr (SPLIT == 2) {
     float* part = red + TPC * WARPS * NB * 4 * 32;                        // [NB*128]
     if (half == 1 && threadIdx.x < NB * 128) part[threadIdx.x] = v;
@@ -319,11 +342,18 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
     const int n = rt * 16 + row;
     if (n < a.N && tok < a.M) epi_apply<T>(a.e, tok, n, v);
   }
+  if (trace) {
+    ts[6] = gtime();
+    const unsigned i = atomicAdd(&g_ktrace_n, 1u) & 4095u;
+    for (int k = 0; k < 6; ++k) g_ktrace[i][k] = ts[k + 1] - ts[0];
+    g_ktrace[i][6] = a.N;
+    g_ktrace[i][7] = a.ks * 16 + (LN ? 100000 : 0);
+  }
 }
 
-template <typename T, int NB, int KW, bool LN, int NV, int SPLIT = 1, int TPC = 1>
+template <typename T, int NB, int KW, bool LN, int NV, int SPLIT = 1, int TPC = 1, int CL = 1>
 static void go(const Args<T>& a, int rtiles, cudaStream_t st) {
-  auto kern = gemv_mma_kernel<T, NB, KW, LN, NV, SPLIT, TPC>;
+  auto kern = gemv_mma_kernel<T, NB, KW, LN, NV, SPLIT, TPC, CL>;
   const size_t smem = (size_t)16 * (a.ks * 16 / SPLIT + XPAD) * sizeof(T) + (size_t)TPC * WARPS * NB * 4 * 32 * 4 +
                       (LN ? (size_t)2 * a.ks * 16 * 4 : 0) + (SPLIT == 2 ? (size_t)NB * 128 * 4 : 0);
   static size_t set = 0;
@@ -331,7 +361,8 @@ static void go(const Args<T>& a, int rtiles, cudaStream_t st) {
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = smem;
   }
-  launch_ex(kern, dim3((rtiles + TPC - 1) / TPC * SPLIT), dim3(THREADS), smem, st, true, dim3(SPLIT, 1, 1), a);
+  const int ctas = (rtiles + TPC - 1) / TPC * SPLIT;
+  launch_ex(kern, dim3((ctas + CL - 1) / CL * CL), dim3(THREADS), smem, st, true, dim3(SPLIT * CL, 1, 1), a);
   EET_LAUNCH_CHECK();
 }
 
@@ -460,6 +491,31 @@ extern "C" int eet_gemv_packed(int dtype, const void* w, int N, int K, const voi
     e.ldo = N;
     const bool ok = gemv_packed(dtype, w, M, N, K, X, K, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st);
     EET_REQUIRE(ok, EET_ERR_UNSUPPORTED, "gemv_packed: unsupported shape");
+    return EET_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+}  // namespace eet
+
+namespace eet {
+extern "C" int eet_debug_ktrace(int on, long long* out, int* n) {
+  // on = 1: reset + enable; on = 0: disable and copy out (4096 x 8)
+  try {
+    if (on) {
+      const int one = 1;
+      const unsigned zero = 0;
+      EET_CHECK_CUDA(cudaMemcpyToSymbol(gm::g_ktrace_on, &one, sizeof(int)));
+      EET_CHECK_CUDA(cudaMemcpyToSymbol(gm::g_ktrace_n, &zero, sizeof(unsigned)));
+    } else {
+      const int zero = 0;
+      unsigned cnt = 0;
+      EET_CHECK_CUDA(cudaDeviceSynchronize());
+      EET_CHECK_CUDA(cudaMemcpyToSymbol(gm::g_ktrace_on, &zero, sizeof(int)));
+      EET_CHECK_CUDA(cudaMemcpyFromSymbol(&cnt, gm::g_ktrace_n, sizeof(unsigned)));
+      EET_CHECK_CUDA(cudaMemcpyFromSymbol(out, gm::g_ktrace, sizeof(long long) * 4096 * 8));
+      *n = (int)std::min<unsigned>(cnt, 4096u);
+    }
     return EET_OK;
   } catch (const Fail& f) {
     return f.code;

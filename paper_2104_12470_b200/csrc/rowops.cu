@@ -501,4 +501,26 @@ void launch_advance(int* d_filled, int* d_step, cudaStream_t st) {
   EET_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------- launch-chain calibration
+// n back-to-back dependent launches of a (nearly) empty kernel, with or
+// without programmatic dependent launch: the per-link floor of a decode graph
+__global__ void empty_link_kernel(int* p) {
+  sm100::griddep_wait();
+  sm100::griddep_launch_dependents();
+  if (p && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(p, 1);
+}
+
 }  // namespace eet
+
+extern "C" int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream) {
+  try {
+    for (int i = 0; i < n; ++i) {
+      eet::launch_ex(eet::empty_link_kernel, dim3(ctas), dim3(128), 0, reinterpret_cast<cudaStream_t>(stream),
+                     pdl != 0, dim3(1, 1, 1), counter);
+      EET_CHECK_CUDA(cudaGetLastError());
+    }
+    return EET_OK;
+  } catch (const eet::Fail& f) {
+    return f.code;
+  }
+}
