@@ -222,9 +222,11 @@ int decode_splits(int batch, int heads, int smax, int hd, int es);
 // cudaLaunchKernelEx with optional programmatic-dependent-launch edge and
 // cluster shape. Kernels launched with pdl=true must execute
 // griddepcontrol.wait before touching memory written by earlier kernels.
+bool pdl_enabled();                    // EET_NO_PDL=1 turns the PDL edges off (A/B, debugging)
 template <typename... KArgs, typename... Args>
 inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                       bool pdl, dim3 cluster, Args&&... args) {
+  pdl = pdl && pdl_enabled();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

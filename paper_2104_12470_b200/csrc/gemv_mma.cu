@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
   if (trace) ts[1] = gtime();
   sm100::griddep_wait();
   sm100::griddep_launch_dependents();
+  if constexpr (LN) __syncthreads();             // gamma/beta staged by other threads (racecheck)
   if (trace) ts[2] = gtime();
 
   // 2. activation rows -> xs (rows >= M are zero)

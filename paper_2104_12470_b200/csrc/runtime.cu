@@ -18,6 +18,14 @@ static thread_local std::string t_err;
 std::atomic<uint64_t> g_launches{0};
 void set_error(const std::string& msg) { t_err = msg; }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EET_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 bool sync_debug() {
   static const bool on = [] {
     const char* e = std::getenv("EET_SYNC_DEBUG");
