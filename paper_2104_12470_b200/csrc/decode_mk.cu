@@ -640,8 +640,11 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
           const bool ok = jj < kn;
           const uint4* kp = reinterpret_cast<const uint4*>(sl + jj * (HD * 2) + sub * 32);
           const uint4* vp = reinterpret_cast<const uint4*>(sl + SLOT / 2 + jj * (HD * 2) + sub * 32);
-          const uint4 z = make_uint4(0, 0, 0, 0);
-          consume(ok ? kp[0] : z, ok ? kp[1] : z, ok ? vp[0] : z, ok ? vp[1] : z, ok);
+          uint4 k0v = make_uint4(0, 0, 0, 0), k1v = k0v, v0v = k0v, v1v = k0v;
+          if (ok) {                                // no reads past the copied keys
+            k0v = kp[0]; k1v = kp[1]; v0v = vp[0]; v1v = vp[1];
+          }
+          consume(k0v, k1v, v0v, v1v, ok);
           release();
         }
         if (k1 == nb_ && warp == 0) {            // this step's slot, written by LN1+QKV
