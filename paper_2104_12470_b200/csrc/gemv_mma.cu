@@ -44,6 +44,7 @@ struct Args {
   const float* x; long long x_sb, x_ss; const int2* rinfo;   // LN: fp32 rows via row map
   const float* g; const float* b;
   Epi e;
+  int persist;                    // LM head: one wave of CTAs loops over the tiles
 };
 
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
@@ -80,13 +81,12 @@ __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
   return v > bv || (v == bv && i < bi);
 }
 template <typename T>
-__device__ __noinline__ void argmax_tail(const Args<T>& a, const float* red, int NB) {
+__device__ __noinline__ void argmax_tail(const Args<T>& a, const float* red, int NB, int rt) {
   __shared__ float tile[16][17];
   __shared__ float bvs[16][16];
   __shared__ int bis[16][16];
   __shared__ int s_last;
   const Epi& e = a.e;
-  const int rt = blockIdx.x;
   const int step = *e.d_step;
   for (int t = threadIdx.x; t < 256; t += blockDim.x) tile[t >> 4][t & 15] = -INFINITY;
   __syncthreads();
@@ -115,6 +115,7 @@ __device__ __noinline__ void argmax_tail(const Args<T>& a, const float* red, int
       }
     e.cand[rt * 16 + threadIdx.x] = make_int2(__float_as_int(bv), bi);
   }
+  __syncthreads();                                 // tile / red reusable by the next tile
 }
 
 // second stage: one CTA per token reduces the per-tile candidates in id order
@@ -301,9 +302,52 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
 #pragma unroll
       for (int i = 0; i < 4; ++i) red[((u * WARPS + warp) * NB * 4 + nb * 4 + i) * 32 + lane] = acc[u][nb][i];
   __syncthreads();
-  if constexpr (TPC == 1) {
+  if constexpr (TPC == 1 && SPLIT == 1) {
+    if (a.persist) {
+      // LM head: X staged once; this CTA's tiles rt, rt + G, ... with the
+      // next tile's weights in flight while the current one is reduced
+      for (int r = rt; r < rtiles; r += gridDim.x) {
+        const int rn = r + (int)gridDim.x;
+        if (rn < rtiles) {                         // next tile's weights in flight ...
+          const uint4* wp = a.w + ((size_t)rn * a.ks + (size_t)warp * KW) * 32 + lane;
+#pragma unroll
+          for (int i = 0; i < KW; ++i) wv[0][i] = ldg_stream(wp + i * 32);
+        }
+        argmax_tail(a, red, NB, r);                // ... while this one is reduced
+        if (rn >= rtiles) break;
+        float acc2[NB][4];
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc2[nb][i] = 0.f;
+        const int g = lane >> 2, c4 = lane & 3;
+#pragma unroll
+        for (int i = 0; i < KW; ++i) {
+          const int k0 = (warp * KW + i) * 16;
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const T* xr = xs + (nb * 8 + g) * xst + k0 + 2 * c4;
+            mma16816<T>(acc2[nb], wv[0][i], *reinterpret_cast<const uint32_t*>(xr),
+                        *reinterpret_cast<const uint32_t*>(xr + 8));
+          }
+        }
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) red[(warp * NB * 4 + nb * 4 + i) * 32 + lane] = acc2[nb][i];
+        __syncthreads();
+      }
+      return;
+    }
     if (a.e.mode == EPI_ARGMAX) {
-      argmax_tail(a, red, NB);
+      argmax_tail(a, red, NB, rt);
+      if (trace) {
+        ts[4] = ts[5] = ts[6] = gtime();
+        const unsigned i = atomicAdd(&g_ktrace_n, 1u) & 4095u;
+        for (int k = 0; k < 6; ++k) g_ktrace[i][k] = ts[k + 1] - ts[0];
+        g_ktrace[i][6] = a.N;
+        g_ktrace[i][7] = a.ks * 16 + (LN ? 100000 : 0);
+      }
       return;
     }
   }
@@ -362,7 +406,12 @@ static void go(const Args<T>& a, int rtiles, cudaStream_t st) {
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = smem;
   }
-  const int ctas = (rtiles + TPC - 1) / TPC * SPLIT;
+  int ctas = (rtiles + TPC - 1) / TPC * SPLIT;
+  if (a.persist) {                               // one wave
+    int per_sm = 1;
+    EET_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
+    ctas = std::min(ctas, std::max(1, per_sm) * device_sm_count());
+  }
   launch_ex(kern, dim3((ctas + CL - 1) / CL * CL), dim3(THREADS), smem, st, true, dim3(SPLIT * CL, 1, 1), a);
   EET_LAUNCH_CHECK();
 }
@@ -448,10 +497,11 @@ bool gemv_packed(int dtype, const void* wsrc, int M, int N, int K, const void* X
   bool ok2;
   if (dtype == EET_BF16) {
     gm::Args<__nv_bfloat16> a{w, K / 16, N, M, reinterpret_cast<const __nv_bfloat16*>(X), ldx,
-                              x, x_sb, x_ss, rinfo, g, b, e};
+                              x, x_sb, x_ss, rinfo, g, b, e, e.mode == EPI_ARGMAX ? 1 : 0};
     ok2 = M <= 8 ? gm::dispatch<__nv_bfloat16, 1>(a, rtiles, ln, st) : gm::dispatch<__nv_bfloat16, 2>(a, rtiles, ln, st);
   } else {
-    gm::Args<__half> a{w, K / 16, N, M, reinterpret_cast<const __half*>(X), ldx, x, x_sb, x_ss, rinfo, g, b, e};
+    gm::Args<__half> a{w, K / 16, N, M, reinterpret_cast<const __half*>(X), ldx, x, x_sb, x_ss, rinfo, g, b, e,
+                       e.mode == EPI_ARGMAX ? 1 : 0};
     ok2 = M <= 8 ? gm::dispatch<__half, 1>(a, rtiles, ln, st) : gm::dispatch<__half, 2>(a, rtiles, ln, st);
   }
   if (ok2 && e.mode == EPI_ARGMAX) {        // second stage of the fused argmax
