@@ -248,17 +248,17 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
     }
   } else {
     const int w8 = K / 8;                        // 16 B chunks per row
-    for (int base = 0; base < 16 * w8; base += 4 * THREADS) {
-      uint4 v[4];
+    for (int base = 0; base < 16 * w8; base += 8 * THREADS) {   // K <= 1024: one round trip
+      uint4 v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int i = base + u * THREADS + threadIdx.x;
         const int r = i / w8, c = i - r * w8;
         v[u] = (i < 16 * w8 && r < a.M) ? reinterpret_cast<const uint4*>(a.X + (size_t)r * a.ldx + half * K)[c]
                                         : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int i = base + u * THREADS + threadIdx.x;
         const int r = i / w8, c = i - r * w8;
         if (i < 16 * w8) *reinterpret_cast<uint4*>(xs + r * xst + c * 8) = v[u];

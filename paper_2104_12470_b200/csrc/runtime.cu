@@ -489,6 +489,7 @@ struct eet_runtime {
   int* h_prompts = nullptr;           // pinned staging: prompts in, tokens out
   long long* h_tokens = nullptr;
   MkState* mk = nullptr;              // decode megakernel state (packed weights, scratch)
+  float* xdec = nullptr;              // decode residual stream [bmax, h]
   int2* cand = nullptr;               // fused LM-head argmax candidates
   int* cand_ticket = nullptr;
   int cand_cap = 0;
@@ -905,18 +906,23 @@ static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long 
 }
 
 // L_host: keys attended this step when known on the host (-1 under capture)
+// The decode residual stream lives in a compact [b, h] buffer: the activation
+// cache rows (max_prompt * h apart, one 2 MB page each at c2) cost every
+// LN-fused GEMV a TLB walk per row.
 static void decode_iteration(eet_runtime* rt, const eet_model* m, int batch, int steps,
                              long long* d_tokens, float* d_logits, int L_host, cudaStream_t st) {
   const int h = rt->h;
-  const long long x_sb = (long long)m->max_prompt * h;
+  if (!rt->xdec) rt->xdec = (float*)rt->dev(sizeof(float) * (size_t)rt->bmax * h);
+  float* x = rt->xdec;
+  const long long x_sb = h;
   StepPlan& p = rt->plans[2];
-  launch_embed_step(rt->dtype, m->tok_emb, m->pos_emb, rt->d_cur, p.pads, rt->d_filled, m->hidden,
-                    x_sb, batch, h, st);
+  launch_embed_step(rt->dtype, m->tok_emb, m->pos_emb, rt->d_cur, p.pads, rt->d_filled, x, x_sb,
+                    batch, h, st);
   for (int l = 0; l < m->layers; ++l)
-    layer_impl(rt, p, m->hidden, x_sb, h, &m->layer[l], m->kcache[l], m->vcache[l], rt->d_filled,
-               0, true, L_host, st);
+    layer_impl(rt, p, x, x_sb, h, &m->layer[l], m->kcache[l], m->vcache[l], rt->d_filled, 0, true,
+               L_host, st);
   launch_advance(rt->d_filled, rt->d_step, st);
-  head_step(rt, m, m->hidden, x_sb, 0, batch, steps, d_tokens, d_logits, st);
+  head_step(rt, m, x, x_sb, 0, batch, steps, d_tokens, d_logits, st);
 }
 
 int eet_generate(eet_runtime* rt, const eet_model* m, const int* h_prompts, const int* h_lengths,
