@@ -571,275 +571,6 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32) attn_decode_bulk_kernel(Dec
   if (threadIdx.x == 0) a.counters[b * a.heads + head] = 0;
 }
 
-// Balanced key-range decode attention (16-bit, head_dim 64). The keys of
-// all (sequence, head) pairs — pair p = b*heads + head holds cache slots
-// [pad_b, L) — are laid end to end and cut into one contiguous range per CTA
-// (2 CTAs per SM), so every CTA streams the same number of K/V bytes
-// whatever the ragged lengths. A producer warp moves each segment's K and V
-// rows (contiguous in the [b, heads, s_max, hd] cache) through a 4 x 16 KB
-// ring with cp.async.bulk; 8 consumer warps take 8 keys per warp per 64-key
-// chunk (4 lanes x 16 dims per key) with an online softmax
-// (attention.py:138-163 fused with runtime.py:167-178). A pair cut by a
-// range boundary is merged by the CTA that finishes its last piece
-// (acq_rel ticket), pieces in key order: deterministic.
-namespace rng {
-constexpr int RW = 8, KPC = 64, NBUF = 4, HD = 64;
-constexpr int CHUNK = KPC * HD * 2;               // bytes of K (or V) per chunk
-
-__device__ __forceinline__ long long lo_of(long long total, int c, int G) { return total * c / G; }
-__device__ __forceinline__ int owner_of(long long total, long long u, int G) {
-  int c = (int)((u * G) / total);
-  while (c + 1 < G && lo_of(total, c + 1, G) <= u) ++c;
-  while (c > 0 && lo_of(total, c, G) > u) --c;
-  return c;
-}
-__device__ __forceinline__ bool nonempty(long long total, int c, int G) {
-  return lo_of(total, c + 1, G) > lo_of(total, c, G);
-}
-
-template <typename T>
-__device__ __forceinline__ void cvt8(const uint4& r, float* o) {
-  const T* v = reinterpret_cast<const T*>(&r);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) o[i] = to_f(v[i]);
-}
-
-template <typename T>
-__global__ void __launch_bounds__((RW + 1) * 32) attn_decode_range_kernel(DecodeArgs a) {
-  extern __shared__ __align__(128) uint8_t dsm[];
-  uint8_t* ring = dsm;                                          // NBUF x (K chunk | V chunk)
-  int* s_n = reinterpret_cast<int*>(dsm + NBUF * 2 * CHUNK);    // [batch] keys per pair
-  long long* s_off = reinterpret_cast<long long*>(s_n + ((a.batch + 1) & ~1));   // [batch + 1]
-  __shared__ __align__(8) uint64_t full[NBUF], empty[NBUF];
-  __shared__ float red[RW][HD + 2];
-  __shared__ int s_flag;
-  const int G = gridDim.x, cta = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NBUF; ++i) {
-      sm100::mbar_init(&full[i], 1);
-      sm100::mbar_init(&empty[i], RW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  sm100::griddep_wait();                  // K/V of this step were written by the QKV GEMV
-  sm100::griddep_launch_dependents();
-  const int L = (a.kv_start ? *a.kv_start : 0) + a.kv_base + 1;
-  if (threadIdx.x == 0) {
-    long long tot = 0;
-    for (int b = 0; b < a.batch; ++b) {
-      s_n[b] = L - a.pads[b];
-      s_off[b] = tot;
-      tot += (long long)a.heads * s_n[b];
-    }
-    s_off[a.batch] = tot;
-  }
-  __syncthreads();
-  const long long total = s_off[a.batch];
-  const long long lo = lo_of(total, cta, G), hi = lo_of(total, cta + 1, G);
-  // segment walk shared by producer and consumers
-  auto seg = [&](long long k, int& b, int& head, int& k0, int& k1, long long& pstart) {
-    b = 0;
-    while (b + 1 < a.batch && s_off[b + 1] <= k) ++b;
-    const long long rel = k - s_off[b];
-    head = (int)(rel / s_n[b]);
-    k0 = (int)(rel - (long long)head * s_n[b]);
-    pstart = s_off[b] + (long long)head * s_n[b];
-    k1 = (int)(min(hi, pstart + s_n[b]) - pstart);
-  };
-  const T* Kc = reinterpret_cast<const T*>(a.kc);
-  const T* Vc = reinterpret_cast<const T*>(a.vc);
-
-  if (warp == RW) {                       // ---- producer
-    if (lane == 0) {
-      int slot = 0;
-      uint32_t par = 0;
-      for (long long k = lo; k < hi;) {
-        int b, head, k0, k1;
-        long long ps;
-        seg(k, b, head, k0, k1, ps);
-        const size_t base = (((size_t)b * a.heads + head) * a.smax + a.pads[b]) * HD;
-        for (int j = k0; j < k1; j += KPC) {
-          const uint32_t by = (uint32_t)(min(KPC, k1 - j) * HD * sizeof(T));
-          sm100::mbar_wait(&empty[slot], par ^ 1);
-          sm100::mbar_expect_tx(&full[slot], 2 * by);
-          sm100::bulk_load(ring + slot * 2 * CHUNK, Kc + base + (size_t)j * HD, by, &full[slot]);
-          sm100::bulk_load(ring + slot * 2 * CHUNK + CHUNK, Vc + base + (size_t)j * HD, by, &full[slot]);
-          if (++slot == NBUF) { slot = 0; par ^= 1; }
-        }
-        k = ps + k1;
-      }
-    }
-    return;
-  }
-  // ---- consumers: lane group grp (4 lanes) owns one key, lane sub 16 dims
-  const int grp = lane >> 2, sub = lane & 3;
-  int slot = 0;
-  uint32_t par = 0;
-  for (long long k = lo; k < hi;) {
-    int b, head, k0, k1;
-    long long pstart;
-    seg(k, b, head, k0, k1, pstart);
-    const int nb = s_n[b];
-    float q[16];
-    {
-      const uint4* qp = reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(a.q) + (long long)b * a.ldq + head * HD + sub * 16);
-      cvt8<T>(qp[0], q);
-      cvt8<T>(qp[1], q + 8);
-    }
-    float m = -INFINITY, l = 0.f, acc[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-    for (int j = k0; j < k1; j += KPC) {
-      const int kn = min(KPC, k1 - j);
-      sm100::mbar_wait(&full[slot], par);
-      const uint8_t* sk = ring + slot * 2 * CHUNK;
-      const int jj = warp * 8 + grp;
-      const bool ok = jj < kn;
-      float kv[16];
-      if (ok) {
-        const uint4* kp = reinterpret_cast<const uint4*>(sk + jj * (HD * 2) + sub * 32);
-        cvt8<T>(kp[0], kv);
-        cvt8<T>(kp[1], kv + 8);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) kv[e] = 0.f;
-      }
-      float dot = 0.f;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) dot = fmaf(q[e], kv[e], dot);
-      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-      if (ok) {
-        float vv[16];
-        const uint4* vp = reinterpret_cast<const uint4*>(sk + CHUNK + jj * (HD * 2) + sub * 32);
-        cvt8<T>(vp[0], vv);
-        cvt8<T>(vp[1], vv + 8);
-        const float s = dot * a.scale;
-        const float mn = fmaxf(m, s);
-        const float corr = __expf(m - mn);          // m = -inf -> 0
-        const float p = __expf(s - mn);
-        l = l * corr + p;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) acc[e] = fmaf(p, vv[e], acc[e] * corr);
-        m = mn;
-      }
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&empty[slot]);
-      if (++slot == NBUF) { slot = 0; par ^= 1; }
-    }
-    // merge the 8 key groups of the warp, then the warps (in order)
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      const float mo = __shfl_xor_sync(0xffffffffu, m, o);
-      const float lo2 = __shfl_xor_sync(0xffffffffu, l, o);
-      const float mn = fmaxf(m, mo);
-      const float c1 = (m == -INFINITY) ? 0.f : __expf(m - mn);
-      const float c2 = (mo == -INFINITY) ? 0.f : __expf(mo - mn);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) acc[e] = acc[e] * c1 + __shfl_xor_sync(0xffffffffu, acc[e], o) * c2;
-      l = l * c1 + lo2 * c2;
-      m = mn;
-    }
-    if (grp == 0) {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) red[warp][sub * 16 + e] = acc[e];
-      if (sub == 0) { red[warp][HD] = m; red[warp][HD + 1] = l; }
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(RW * 32) : "memory");
-    const bool whole = (k0 == 0 && k1 == nb);
-    const int ct = threadIdx.x;
-    if (ct < HD) {
-      float um = -INFINITY, ul = 0.f, ua = 0.f;
-#pragma unroll
-      for (int w = 0; w < RW; ++w) um = fmaxf(um, red[w][HD]);
-#pragma unroll
-      for (int w = 0; w < RW; ++w) {
-        const float cw = (red[w][HD] == -INFINITY) ? 0.f : __expf(red[w][HD] - um);
-        ul += red[w][HD + 1] * cw;
-        ua += red[w][ct] * cw;
-      }
-      if (whole) {
-        reinterpret_cast<T*>(a.o)[(long long)b * a.ldo + head * HD + ct] = from_f<T>(ua / ul);
-      } else {
-        float* dst = a.part + ((size_t)cta * 2 + (k0 > 0 ? 0 : 1)) * (HD + 2);
-        dst[ct] = ua;
-        if (ct == 0) { dst[HD] = um; dst[HD + 1] = ul; }
-      }
-    }
-    asm volatile("bar.sync 1, %0;" ::"n"(RW * 32) : "memory");
-    if (!whole) {
-      if (ct == 0) {
-        const int c0 = owner_of(total, pstart, G), c1 = owner_of(total, pstart + nb - 1, G);
-        int pieces = 0;
-        for (int cc = c0; cc <= c1; ++cc) pieces += nonempty(total, cc, G);
-        int prev;
-        int* ctr = a.counters + (b * a.heads + head);
-        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(prev) : "l"(ctr) : "memory");
-        s_flag = (prev == pieces - 1) ? (c0 << 16) | c1 : -1;
-        if (s_flag >= 0) *ctr = 0;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(RW * 32) : "memory");
-      const int f = s_flag;
-      if (f >= 0 && ct < HD) {
-        const int c0 = f >> 16, c1 = f & 0xffff;
-        float M = -INFINITY;
-        for (int cc = c0; cc <= c1; ++cc)
-          if (nonempty(total, cc, G)) M = fmaxf(M, __ldcg(a.part + ((size_t)cc * 2 + (cc == c0)) * (HD + 2) + HD));
-        float Ls = 0.f, A = 0.f;
-        for (int cc = c0; cc <= c1; ++cc) {
-          if (!nonempty(total, cc, G)) continue;
-          const float* src = a.part + ((size_t)cc * 2 + (cc == c0)) * (HD + 2);
-          const float ms = __ldcg(src + HD);
-          const float cw = (ms == -INFINITY) ? 0.f : __expf(ms - M);
-          Ls += __ldcg(src + HD + 1) * cw;
-          A += __ldcg(src + ct) * cw;
-        }
-        reinterpret_cast<T*>(a.o)[(long long)b * a.ldo + head * HD + ct] = from_f<T>(A / Ls);
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(RW * 32) : "memory");
-    }
-    k = pstart + k1;
-  }
-}
-}  // namespace rng
-
-int decode_range_ctas() { return 2 * device_sm_count(); }
-
-static bool decode_range_launch(const DecodeArgs& a, cudaStream_t st) {
-  static const bool on = [] {                   // A/B switch (default: per-pair streaming kernel)
-    const char* e = std::getenv("EET_ATTN_RANGE");
-    return e && e[0] == '1';
-  }();
-  if (!on || a.hd != rng::HD || a.dtype == EET_F32 || a.ldq % 8 || a.ldo % 8 ||
-      ((reinterpret_cast<uintptr_t>(a.kc) | reinterpret_cast<uintptr_t>(a.vc) |
-        reinterpret_cast<uintptr_t>(a.q)) & 15))
-    return false;
-  // one wave (2 CTAs per SM at ~100 registers), and >= ~512 keys per CTA at
-  // the cache capacity so small batches are not shredded into tiny pieces
-  const long long cap_keys = (long long)a.batch * a.heads * a.smax;
-  const int G = (int)std::max<long long>(1, std::min<long long>(decode_range_ctas(), (cap_keys + 511) / 512));
-  const size_t smem = (size_t)rng::NBUF * 2 * rng::CHUNK + sizeof(int) * ((a.batch + 2) & ~1) +
-                      sizeof(long long) * (a.batch + 1);
-  double keys = 0;
-  for (int b = 0; b < a.batch; ++b) keys += (a.L_host >= 0 ? a.L_host : a.smax) - (a.h_pads ? a.h_pads[b] : 0);
-  const double es = 2.0;
-  const double per_key_b = (double)a.heads * a.hd * 2 * es, per_key_f = (double)a.heads * 4.0 * a.hd;
-  if (a.L_host < 0) keys = 0;
-  ProfScope ps(K_ATTN_DECODE, st, keys * per_key_b + 2.0 * a.batch * a.heads * a.hd * es, keys * per_key_f,
-               a.L_host >= 0 ? 0.0 : per_key_b, a.L_host >= 0 ? 0.0 : per_key_f);
-  auto go = [&](auto kern) {
-    EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_ex(kern, dim3(G), dim3((rng::RW + 1) * 32), smem, st, true, dim3(1, 1, 1), a);
-  };
-  if (a.dtype == EET_BF16) go(rng::attn_decode_range_kernel<__nv_bfloat16>);
-  else go(rng::attn_decode_range_kernel<__half>);
-  EET_LAUNCH_CHECK();
-  return true;
-}
-
-// Splits per (b, head): ~128 keys per CTA (32 per warp = one batch of
-// in-flight loads) and at least ~2 CTAs per SM for small batches.
 int decode_splits(int batch, int heads, int smax, int hd, int es) {
   (void)hd; (void)es;
   // one wave of the streaming kernel (3 CTAs of 64 KB ring per SM): a
@@ -873,13 +604,10 @@ static void decode_bulk_launch_n(const DecodeArgs& a, cudaStream_t st);
 
 template <typename T, int E, int LPK>
 static void decode_bulk_launch(const DecodeArgs& a, cudaStream_t st) {
-  constexpr int NB0 = (E * LPK * sizeof(T) <= 128) ? 4 : 2;    // ring <= 64 KB
-  static const int deep = [] {                                  // A/B: 6-chunk ring
-    const char* e = std::getenv("EET_ATTN_NBUF6");
-    return (e && e[0] == '1') ? 1 : 0;
-  }();
-  if (NB0 == 4 && deep) return decode_bulk_launch_n<T, E, LPK, 6>(a, st);
-  return decode_bulk_launch_n<T, E, LPK, NB0>(a, st);
+  // 4 x 16 KB ring (<= 64 KB): 2 CTAs per SM stay co-resident with the
+  // neighbouring GEMVs under PDL (a 6-deep ring measured slower, r01)
+  constexpr int NBUF = (E * LPK * sizeof(T) <= 128) ? 4 : 2;
+  decode_bulk_launch_n<T, E, LPK, NBUF>(a, st);
 }
 
 template <typename T, int E, int LPK, int NBUF>
@@ -953,7 +681,6 @@ static void decode_dispatch(const DecodeArgs& a, cudaStream_t st) {
 
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st) {
   if (a.batch <= 0) return;
-  if (decode_range_launch(a, st)) return;
   switch (a.dtype) {
     case EET_F32: decode_dispatch<float>(a, st); break;
     case EET_BF16: decode_dispatch<__nv_bfloat16>(a, st); break;

@@ -195,7 +195,6 @@ struct DecodeArgs {
   int splits;
 };
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
-int decode_range_ctas();               // CTAs of the key-range decode kernel (part: 2 slots each)
 
 // ---- decode GEMV from pre-permuted weights (gemv_mma.cu)
 void packed_register(const void* src, const void* packed);

@@ -154,34 +154,26 @@ __global__ void __launch_bounds__(256) argmax_cand_kernel(const int2* __restrict
 
 // NB n-blocks of 8 token rows; KW fragments per warp (K = 16 * 8 * KW);
 // NV float4 per lane per LayerNorm row (h <= 128 * NV)
-// SPLIT = 2: a 2-CTA cluster shares one tile, each CTA half of K, and the
-// halves are summed through distributed shared memory (rank 0 + rank 1).
-template <typename T, int NB, int KW, bool LN, int NV, int SPLIT, int TPC, int CL = 1>
+template <typename T, int NB, int KW, bool LN, int NV>
 __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant__ Args<T> a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int K = a.ks * 16 / SPLIT, xst = K + XPAD;                      // K: this CTA's span
+  const int K = a.ks * 16, xst = K + XPAD;
   T* xs = reinterpret_cast<T*>(smem);                                   // [16][K + XPAD]
-  float* red = reinterpret_cast<float*>(smem + (size_t)16 * xst * sizeof(T));   // [TPC][WARPS][NB*4][32]
-  // TPC tiles per CTA (TPC = 2: the staged activation rows serve twice the
-  // weight rows); SPLIT = 2: one tile over a 2-CTA cluster
-  const int rt = (blockIdx.x / SPLIT) * TPC, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = SPLIT == 2 ? (int)sm100::cluster_ctarank() : 0;
+  float* red = reinterpret_cast<float*>(smem + (size_t)16 * xst * sizeof(T));   // [WARPS][NB*4][32]
+  const int rt = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rtiles = (a.N + 15) / 16;
-
   const bool trace = g_ktrace_on && blockIdx.x == 0 && threadIdx.x == 0;
   long long ts[7];
   if (trace) ts[0] = gtime();
   // 1. this warp's weight slice -> registers (static data: before the wait)
-  uint4 wv[TPC][KW];
+  uint4 wv[KW];
+  {
+    const uint4* wp = a.w + ((size_t)rt * a.ks + (size_t)warp * KW) * 32 + lane;
 #pragma unroll
-  for (int u = 0; u < TPC; ++u) {
-    const uint4* wp = a.w + ((size_t)(rt + u) * a.ks + (size_t)half * (a.ks / SPLIT) + (size_t)warp * KW) * 32 + lane;
-    const bool ok = rt + u < rtiles;
-#pragma unroll
-    for (int i = 0; i < KW; ++i) wv[u][i] = ok ? ldg_stream(wp + i * 32) : make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < KW; ++i) wv[i] = ldg_stream(wp + i * 32);
   }
   // LayerNorm gamma/beta are static too: stage them in shared memory now
-  float* sgb = red + TPC * WARPS * NB * 4 * 32;                          // [2][K] (LN only)
+  float* sgb = red + WARPS * NB * 4 * 32;                                // [2][K] (LN only)
   if constexpr (LN) {
     for (int i = threadIdx.x; i < K / 4; i += THREADS) {
       reinterpret_cast<float4*>(sgb)[i] = __ldg(reinterpret_cast<const float4*>(a.g) + i);
@@ -280,7 +272,7 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
       for (int u = 0; u < 8; ++u) {
         const int i = base + u * THREADS + threadIdx.x;
         const int r = i / w8, c = i - r * w8;
-        v[u] = (i < 16 * w8 && r < a.M) ? reinterpret_cast<const uint4*>(a.X + (size_t)r * a.ldx + half * K)[c]
+        v[u] = (i < 16 * w8 && r < a.M) ? reinterpret_cast<const uint4*>(a.X + (size_t)r * a.ldx)[c]
                                         : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
@@ -295,13 +287,11 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
   if (trace) ts[3] = gtime();
 
   // 3. this warp's K slice on the tensor cores
-  float acc[TPC][NB][4];
+  float acc[NB][4];
 #pragma unroll
-  for (int u = 0; u < TPC; ++u)
+  for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) acc[u][nb][i] = 0.f;
+    for (int i = 0; i < 4; ++i) acc[nb][i] = 0.f;
   {
     const int g = lane >> 2, c4 = lane & 3;
 #pragma unroll
@@ -310,25 +300,22 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
         const T* xr = xs + (nb * 8 + g) * xst + k0 + 2 * c4;
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xr), b1 = *reinterpret_cast<const uint32_t*>(xr + 8);
-#pragma unroll
-        for (int u = 0; u < TPC; ++u) mma16816<T>(acc[u][nb], wv[u][i], b0, b1);
+        mma16816<T>(acc[nb], wv[i], *reinterpret_cast<const uint32_t*>(xr),
+                    *reinterpret_cast<const uint32_t*>(xr + 8));
       }
     }
   }
   if (trace && !LN) {
-    float z = acc[0][0][0];                     // MMA results materialised
+    float z = acc[0][0];                        // MMA results materialised
     if (z == 1.2345e-38f) ts[4] = 0; else ts[4] = gtime();
   }
   // 4. warp-ordered reduction + epilogue
 #pragma unroll
-  for (int u = 0; u < TPC; ++u)
+  for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) red[((u * WARPS + warp) * NB * 4 + nb * 4 + i) * 32 + lane] = acc[u][nb][i];
+    for (int i = 0; i < 4; ++i) red[(warp * NB * 4 + nb * 4 + i) * 32 + lane] = acc[nb][i];
   __syncthreads();
-  if constexpr (TPC == 1 && SPLIT == 1) {
+  {
     if (a.persist) {
       // LM head: X staged once; this CTA's tiles rt, rt + G, ... with the
       // next tile's weights in flight while the current one is reduced
@@ -337,7 +324,7 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
         if (rn < rtiles) {                         // next tile's weights in flight ...
           const uint4* wp = a.w + ((size_t)rn * a.ks + (size_t)warp * KW) * 32 + lane;
 #pragma unroll
-          for (int i = 0; i < KW; ++i) wv[0][i] = ldg_stream(wp + i * 32);
+          for (int i = 0; i < KW; ++i) wv[i] = ldg_stream(wp + i * 32);
         }
         argmax_tail(a, red, NB, r);                // ... while this one is reduced
         if (rn >= rtiles) break;
@@ -353,7 +340,7 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
             const T* xr = xs + (nb * 8 + g) * xst + k0 + 2 * c4;
-            mma16816<T>(acc2[nb], wv[0][i], *reinterpret_cast<const uint32_t*>(xr),
+            mma16816<T>(acc2[nb], wv[i], *reinterpret_cast<const uint32_t*>(xr),
                         *reinterpret_cast<const uint32_t*>(xr + 8));
           }
         }
@@ -377,34 +364,12 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
       return;
     }
   }
-  if constexpr (TPC > 1) {
-    for (int t = threadIdx.x; t < TPC * NB * 128; t += THREADS) {
-      const int u = t / (NB * 128), e = t - u * NB * 128;
-      float v = 0.f;
-#pragma unroll
-      for (int w = 0; w < WARPS; ++w) v += red[((u * WARPS + w) * NB * 4) * 32 + e];
-      const int i = e >> 5, ln = e & 31;
-      const int row = (ln >> 2) + 8 * ((i & 3) >> 1);
-      const int tok = (i >> 2) * 8 + 2 * (ln & 3) + (i & 1);
-      const int n = (rt + u) * 16 + row;
-      if (n < a.N && tok < a.M) epi_apply<T>(a.e, tok, n, v);
-    }
-    return;
-  }
   float v = 0.f;
   if (threadIdx.x < NB * 128) {
 #pragma unroll
     for (int w = 0; w < WARPS; ++w) v += red[(w * NB * 4) * 32 + threadIdx.x];
   }
   if (trace && !LN) ts[5] = gtime();
-  if constexpr (SPLIT == 2) {
-    float* part = red + TPC * WARPS * NB * 4 * 32;                        // [NB*128]
-    if (half == 1 && threadIdx.x < NB * 128) part[threadIdx.x] = v;
-    sm100::cluster_sync();
-    if (half == 0 && threadIdx.x < NB * 128) v += sm100::map_peer(part, 1)[threadIdx.x];
-    sm100::cluster_sync();                                                // peer smem stays live
-    if (half == 1) return;
-  }
   if (threadIdx.x < NB * 128) {
     const int e = threadIdx.x;
     const int i = e >> 5, ln = e & 31;
@@ -422,35 +387,30 @@ __global__ void __launch_bounds__(THREADS) gemv_mma_kernel(const __grid_constant
   }
 }
 
-template <typename T, int NB, int KW, bool LN, int NV, int SPLIT = 1, int TPC = 1, int CL = 1>
+template <typename T, int NB, int KW, bool LN, int NV>
 static void go(const Args<T>& a, int rtiles, cudaStream_t st) {
-  auto kern = gemv_mma_kernel<T, NB, KW, LN, NV, SPLIT, TPC, CL>;
-  const size_t smem = (size_t)16 * (a.ks * 16 / SPLIT + XPAD) * sizeof(T) + (size_t)TPC * WARPS * NB * 4 * 32 * 4 +
-                      (LN ? (size_t)2 * a.ks * 16 * 4 : 0) + (SPLIT == 2 ? (size_t)NB * 128 * 4 : 0);
+  auto kern = gemv_mma_kernel<T, NB, KW, LN, NV>;
+  const size_t smem = (size_t)16 * (a.ks * 16 + XPAD) * sizeof(T) + (size_t)WARPS * NB * 4 * 32 * 4 +
+                      (LN ? (size_t)2 * a.ks * 16 * 4 : 0);
   static size_t set = 0;
   if (set < smem) {
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     set = smem;
   }
-  int ctas = (rtiles + TPC - 1) / TPC * SPLIT;
+  int ctas = rtiles;
   if (a.persist) {                               // one wave
     int per_sm = 1;
     EET_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
     ctas = std::min(ctas, std::max(1, per_sm) * device_sm_count());
   }
-  launch_ex(kern, dim3((ctas + CL - 1) / CL * CL), dim3(THREADS), smem, st, true, dim3(SPLIT * CL, 1, 1), a);
+  launch_ex(kern, dim3(ctas), dim3(THREADS), smem, st, true, dim3(1, 1, 1), a);
   EET_LAUNCH_CHECK();
 }
 
 template <typename T, int NB>
 static bool dispatch(const Args<T>& a, int rtiles, bool ln, cudaStream_t st) {
   const int K = a.ks * 16;
-  static const int tpc2 = [] {                  // A/B: two tiles per CTA on the LN GEMVs
-    const char* e = std::getenv("EET_GEMV_TPC2");
-    return (e && e[0] == '1') ? 1 : 0;
-  }();
   if (ln) {
-    if (K == 1024 && tpc2 && a.e.mode != EPI_ARGMAX) { go<T, NB, 8, true, 8, 1, 2>(a, rtiles, st); return true; }
     if (K == 1024) { go<T, NB, 8, true, 8>(a, rtiles, st); return true; }
     if (K == 768) { go<T, NB, 6, true, 6>(a, rtiles, st); return true; }
     if (K == 512) { go<T, NB, 4, true, 4>(a, rtiles, st); return true; }
@@ -464,7 +424,7 @@ static bool dispatch(const Args<T>& a, int rtiles, bool ln, cudaStream_t st) {
     case 1024: go<T, NB, 8, false, 1>(a, rtiles, st); return true;
     case 2048: go<T, NB, 16, false, 1>(a, rtiles, st); return true;
     case 3072: go<T, NB, 24, false, 1>(a, rtiles, st); return true;
-    case 4096: go<T, NB, 16, false, 1, 2>(a, rtiles, st); return true;      // 2-CTA K split
+    case 4096: go<T, NB, 32, false, 1>(a, rtiles, st); return true;
     default: return false;
   }
 }
@@ -511,8 +471,8 @@ bool gemv_packed(int dtype, const void* wsrc, int M, int N, int K, const void* X
     return false;
   if (!ln && ((reinterpret_cast<uintptr_t>(X) & 15) || (ldx % 8))) return false;
   // K > 1024 (W2) stays on the tcgen05 split-K kernel: in the decode graph
-  // it costs 6.7 us per layer vs 7.2 us for the 2-CTA-cluster packed variant
-  // (SPLIT = 2 below) and ~7.2 us for one CTA per tile (r01 A/B)
+  // it costs 6.7 us per layer vs ~7.2 us for one CTA per tile or a 2-CTA
+  // cluster K split of this kernel (r01 A/B)
   const int kl[] = {256, 512, 768, 1024}, kp[] = {256, 512, 768, 1024};
   bool ok = false;
   if (ln) { for (int k : kl) ok |= K == k; } else { for (int k : kp) ok |= K == k; }

@@ -733,9 +733,7 @@ static eet_runtime* runtime_new(int dtype, int hidden, int heads_total, int tp_r
   rt->pool = pool;
   rt->splits = decode_splits(max_batch, heads, max_sequence, rt->hd, (int)dtype_size(dtype));
   for (auto& p : rt->plans) plan_alloc(rt.get(), p);
-  rt->part = (float*)rt->dev(sizeof(float) *
-                             std::max((size_t)max_batch * heads * rt->splits, (size_t)2 * decode_range_ctas()) *
-                             (rt->hd + 2));
+  rt->part = (float*)rt->dev(sizeof(float) * (size_t)max_batch * heads * rt->splits * (rt->hd + 2));
   rt->counters = (int*)rt->dev(sizeof(int) * (size_t)max_batch * heads);
   EET_CHECK_CUDA(cudaMemset(rt->counters, 0, sizeof(int) * (size_t)max_batch * heads));
   rt->d_prompts = (int*)rt->dev(sizeof(int) * (size_t)max_batch * max_sequence);

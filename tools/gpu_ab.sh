@@ -3,4 +3,3 @@ timeout 300 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail 
 timeout 200 python tools/race_probe.py 2>&1 | head -1
 timeout 200 python tools/decode_step_time.py | sed "s/^/full /"
 B=1 timeout 200 python tools/decode_step_time.py | sed "s/^/full /"
-timeout 100 python tools/ktrace.py
