@@ -21,6 +21,8 @@
 #include "sm100.cuh"
 
 #include <cstdlib>
+#include <algorithm>
+#include <vector>
 
 namespace eet {
 namespace fa {
@@ -161,17 +163,38 @@ struct FaArgs {
   int batch, seq, heads, smax, causal;
   float scale_log2;         // (1/sqrt(hd)) * log2(e)
   int poly;                 // polynomial exp2 for half of the keys of full tiles
+  int nitems;               // > 0: CTA i runs work item i / heads (longest first)
+};
+
+// Work list for ragged batches: one entry per non-empty (sequence, query-tile
+// pair), sorted by descending key-tile count on the host, so the block
+// scheduler issues the longest CTAs first (LPT) and never launches CTAs that
+// lie entirely in the padding. Passed by value: no host->device copy to
+// order against the stream, and the launch stays graph-capturable.
+constexpr int MAX_ITEMS = 8192;
+struct FaItems {
+  unsigned short v[MAX_ITEMS];   // (b << 6) | pair
 };
 
 template <typename T, int HD>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
-                   const __grid_constant__ CUtensorMap mapV, FaArgs a) {
+                   const __grid_constant__ CUtensorMap mapV, FaArgs a,
+                   const __grid_constant__ FaItems items) {
   using C = Cfg<HD>;
   constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
-  const int b = blockIdx.z, head = blockIdx.y;
-  const int npair = gridDim.x;
-  const int pair = npair - 1 - blockIdx.x;                // heaviest (latest) queries first
+  int b, head, pair;
+  if (a.nitems > 0) {
+    const int i = blockIdx.x / a.heads;
+    head = blockIdx.x - i * a.heads;
+    const unsigned it = items.v[i];
+    b = (int)(it >> 6);
+    pair = (int)(it & 63u);
+  } else {
+    b = blockIdx.z;
+    head = blockIdx.y;
+    pair = gridDim.x - 1 - blockIdx.x;                    // heaviest (latest) queries first
+  }
   const int q0 = pair * 2 * BQ;
   const int pad = a.pads[b];
   const int qhiA = min(q0 + BQ, a.seq), qhiB = min(q0 + 2 * BQ, a.seq);
@@ -495,9 +518,35 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr = true;
   }
-  dim3 grid((p.seq + 2 * BQ - 1) / (2 * BQ), p.heads, p.batch);
+  const int npair = (p.seq + 2 * BQ - 1) / (2 * BQ);
+  static FaItems items;
+  a.nitems = 0;
+  static const bool no_list = std::getenv("EET_ATTN_GRID") != nullptr;   // A/B switch
+  if (p.h_pads && !no_list && npair <= 64 && p.batch <= 1024 && (long long)p.batch * npair <= MAX_ITEMS) {
+    // cost of a pair = key tiles of its two query tiles (0 when in the padding)
+    static std::vector<std::pair<int, int>> work;
+    work.clear();
+    for (int b = 0; b < p.batch; ++b) {
+      const int pad = p.h_pads[b];
+      for (int pr = npair - 1; pr >= 0; --pr) {
+        const int q0 = pr * 2 * BQ;
+        const int qhiA = std::min(q0 + BQ, p.seq), qhiB = std::min(q0 + 2 * BQ, p.seq);
+        if (qhiB <= pad) continue;
+        const bool liveA = qhiA > pad && q0 < p.seq;
+        const int kA = p.causal ? qhiA : p.seq, kB = p.causal ? qhiB : p.seq;
+        const int cost = (liveA ? (kA - pad + BKV - 1) / BKV : 0) + (kB - pad + BKV - 1) / BKV;
+        work.emplace_back(cost, (b << 6) | pr);
+      }
+    }
+    std::stable_sort(work.begin(), work.end(),
+                     [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first > y.first; });
+    for (size_t i = 0; i < work.size(); ++i) items.v[i] = (unsigned short)work[i].second;
+    a.nitems = (int)work.size();
+    if (a.nitems == 0) return;
+  }
+  dim3 grid = a.nitems > 0 ? dim3((unsigned)(a.nitems * p.heads), 1, 1) : dim3(npair, p.heads, p.batch);
   ProfScope ps(K_ATTN_PREFILL, st, bytes, flops);
-  kern<<<grid, THREADS, C::SMEM, st>>>(mq, mk, mv, a);
+  kern<<<grid, THREADS, C::SMEM, st>>>(mq, mk, mv, a, items);
   EET_LAUNCH_CHECK();
 }
 
