@@ -163,17 +163,18 @@ struct FaArgs {
   int batch, seq, heads, smax, causal;
   float scale_log2;         // (1/sqrt(hd)) * log2(e)
   int poly;                 // polynomial exp2 for half of the keys of full tiles
-  int nitems;               // > 0: CTA i runs work item i / heads (longest first)
+  int nitems;               // > 0: persistent CTAs walk the work list
+  int* ctr;                 // [2] next list entry, CTAs done (zero between launches)
 };
 
-// Work list for ragged batches: one entry per non-empty (sequence, query-tile
-// pair), sorted by descending key-tile count on the host, so the block
-// scheduler issues the longest CTAs first (LPT) and never launches CTAs that
-// lie entirely in the padding. Passed by value: no host->device copy to
-// order against the stream, and the launch stays graph-capturable.
-constexpr int MAX_ITEMS = 8192;
+// Work list: one entry per non-empty (sequence, head, query-tile pair),
+// (sequence, head) groups longest sequence first, the pairs of a group
+// heaviest first and adjacent so they share the group's K/V through L2.
+// Padding-only pairs are never visited. Passed by value: no host->device
+// copy to order against the stream, and the launch stays graph-capturable.
+constexpr int MAX_ITEMS = 7680;                 // kernel parameter space is 32 KB
 struct FaItems {
-  unsigned short v[MAX_ITEMS];   // (b << 6) | pair
+  uint32_t v[MAX_ITEMS];                        // b << 16 | head << 8 | pair
 };
 
 template <typename T, int HD>
@@ -183,27 +184,39 @@ __global__ void __launch_bounds__(THREADS, 1)
                    const __grid_constant__ FaItems items) {
   using C = Cfg<HD>;
   constexpr bool BF = std::is_same<T, __nv_bfloat16>::value;
-  int b, head, pair;
-  if (a.nitems > 0) {
-    const int i = blockIdx.x / a.heads;
-    head = blockIdx.x - i * a.heads;
-    const unsigned it = items.v[i];
-    b = (int)(it >> 6);
-    pair = (int)(it & 63u);
-  } else {
-    b = blockIdx.z;
-    head = blockIdx.y;
-    pair = gridDim.x - 1 - blockIdx.x;                    // heaviest (latest) queries first
+  // Items: with a work list the CTAs are persistent and take list entries
+  // from a global counter (greedy, in list order); without one, the CTA runs
+  // the single (pair, head, b) of its block index.
+  const int n_work = a.nitems;
+  struct Item { int b, head, q0, pad, ntA, ntB; };
+  auto decode = [&](int lin, Item& w) -> bool {
+    int pair;
+    if (n_work > 0) {
+      if (lin >= n_work) return false;
+      const uint32_t it = items.v[lin];
+      w.b = (int)(it >> 16);
+      w.head = (int)((it >> 8) & 255u);
+      pair = (int)(it & 255u);
+    } else {
+      if (lin != 0) return false;
+      w.b = blockIdx.z;
+      w.head = blockIdx.y;
+      pair = gridDim.x - 1 - blockIdx.x;                  // heaviest (latest) queries first
+    }
+    w.q0 = pair * 2 * BQ;
+    w.pad = a.pads[w.b];
+    const int qhiA = min(w.q0 + BQ, a.seq), qhiB = min(w.q0 + 2 * BQ, a.seq);
+    if (qhiB <= w.pad) return false;                      // both tiles in the padding
+    const bool liveA = qhiA > w.pad && w.q0 < a.seq;
+    const int kendA = a.causal ? qhiA : a.seq, kendB = a.causal ? qhiB : a.seq;
+    w.ntA = liveA ? (kendA - w.pad + BKV - 1) / BKV : 0;
+    w.ntB = (kendB - w.pad + BKV - 1) / BKV;              // B's range covers A's
+    return true;
+  };
+  if (n_work == 0) {
+    Item w0;
+    if (!decode(0, w0)) return;
   }
-  const int q0 = pair * 2 * BQ;
-  const int pad = a.pads[b];
-  const int qhiA = min(q0 + BQ, a.seq), qhiB = min(q0 + 2 * BQ, a.seq);
-  if (qhiB <= pad) return;                                // both tiles in the padding
-  const bool liveA = qhiA > pad && q0 < a.seq;
-  const int kendA = a.causal ? qhiA : a.seq, kendB = a.causal ? qhiB : a.seq;
-  const int ntA = liveA ? (kendA - pad + BKV - 1) / BKV : 0;
-  const int ntB = (kendB - pad + BKV - 1) / BKV;          // B's range covers A's
-  const int nt = ntB;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -219,11 +232,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* s_full = bars + 1 + 2 * NST;     // [2 tiles][2 buffers]
   uint64_t* p_full = s_full + 4;             // [2 tiles][2 P buffers]: P(j) in buffer j & 1
   uint64_t* o_done = p_full + 4;             // [2 tiles][2 P buffers]: PV(j) on buffer j & 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 4);
+  uint64_t* q_empty = o_done + 4;
+  uint64_t* it_full = o_done + 5;            // [2] item ring: producer -> MMA / softmax
+  uint64_t* it_empty = o_done + 7;           // [2]
+  int* item_buf = reinterpret_cast<int*>(o_done + 9);     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 10);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&it_full[i], 1);
+      mbar_init(&it_empty[i], 1 + 2 * 4);                 // MMA thread + 8 softmax warps
+    }
     for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
@@ -245,24 +267,36 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int kv_row0 = (b * a.heads + head) * a.smax;      // cache row of slot 0
-
+  // Barrier phases run on across items: K/V stages on the global tile
+  // counter g, S/P/O buffers on per-query-tile counters, Q on the round r
+  // (q_empty: the previous item's S MMAs have finished reading sQ).
   if (warp == NSM) {
     if (lane == 0) {
       const uint64_t pol = 0x14F0000000000000ull;         // EVICT_LAST: K/V reused by query tiles
-      mbar_expect_tx(q_full, 2 * C::Q_BYTES);
-      for (int t = 0; t < 2; ++t)
-        for (int s = 0; s < C::KSUB; ++s)
-          tma_load_2d(sQ + t * C::Q_BYTES + s * C::QSUB, &mapQ, q_full, head * HD + 64 * s,
-                      a.q_rowbase[b] + q0 + t * BQ, pol);
-      for (int j = 0; j < nt; ++j) {
-        const int st = j % NST;
-        mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
-        const int row = kv_row0 + pad + j * BKV;
-        for (int s = 0; s < C::KSUB; ++s) {
-          tma_load_2d(sK + st * C::KV_BYTES + s * C::KVSUB, &mapK, &kv_full[st], 64 * s, row, pol);
-          tma_load_2d(sV + st * C::KV_BYTES + s * C::KVSUB, &mapV, &kv_full[st], 64 * s, row, pol);
+      int g = 0;
+      for (int r = 0;; ++r) {
+        if (r > 0) mbar_wait(q_empty, (r - 1) & 1);       // sQ free; fetch the next item late
+        const int lin = n_work > 0 ? atomicAdd(a.ctr, 1) : (r == 0 ? 0 : 1);
+        if (r >= 2) mbar_wait(&it_empty[r & 1], ((r - 2) >> 1) & 1);
+        item_buf[r & 1] = lin;
+        mbar_arrive(&it_full[r & 1]);
+        Item w;
+        if (!decode(lin, w)) break;
+        mbar_expect_tx(q_full, 2 * C::Q_BYTES);
+        for (int t = 0; t < 2; ++t)
+          for (int s = 0; s < C::KSUB; ++s)
+            tma_load_2d(sQ + t * C::Q_BYTES + s * C::QSUB, &mapQ, q_full, w.head * HD + 64 * s,
+                        a.q_rowbase[w.b] + w.q0 + t * BQ, pol);
+        const int kv_row0 = (w.b * a.heads + w.head) * a.smax;   // cache row of slot 0
+        for (int j = 0; j < w.ntB; ++j, ++g) {
+          const int st = g % NST;
+          mbar_wait(&kv_empty[st], ((g / NST) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
+          const int row = kv_row0 + w.pad + j * BKV;
+          for (int s = 0; s < C::KSUB; ++s) {
+            tma_load_2d(sK + st * C::KV_BYTES + s * C::KVSUB, &mapK, &kv_full[st], 64 * s, row, pol);
+            tma_load_2d(sV + st * C::KV_BYTES + s * C::KVSUB, &mapV, &kv_full[st], 64 * s, row, pol);
+          }
         }
       }
     }
@@ -271,61 +305,79 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t fmt = BF ? 1 : 0;
       constexpr uint32_t id_s = instr_desc(fmt, BQ, BKV);
       constexpr uint32_t id_o = instr_desc(fmt, BQ, HD) | (1u << 16);   // B (V) MN-major
-      mbar_wait(q_full, 0);
-      // Ping-pong: while the softmax warps of one query tile work on S(j),
-      // the tensor core runs the other tile's PV(j) and S(j+1); S_t(j+1) is
-      // issued as soon as tile t's softmax has released S_t(j).
-      auto issue_s = [&](int t, int j) {
-        const uint32_t k_base = smem_u32(sK + (j % NST) * C::KV_BYTES);
-        const uint32_t q_base = smem_u32(sQ + t * C::Q_BYTES);
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t qoff = (k >> 2) * C::QSUB + (k & 3) * 32;
-          const uint32_t koff = (k >> 2) * C::KVSUB + (k & 3) * 32;
-          mma_f16(tmem + C::S_COL + (t * 2 + (j & 1)) * BKV, smem_desc(q_base + qoff),
-                  smem_desc(k_base + koff), id_s, k > 0);
-        }
-        mma_commit(&s_full[t * 2 + (j & 1)]);
-      };
-      auto issue_o = [&](int t, int j) {
-        mbar_wait(&p_full[t * 2 + (j & 1)], (j >> 1) & 1);
+      int g0 = 0, cA = 0, cB = 0;                         // item-start counters
+      for (int r = 0;; ++r) {
+        mbar_wait(&it_full[r & 1], (r >> 1) & 1);
+        const int lin = *reinterpret_cast<volatile int*>(&item_buf[r & 1]);
+        mbar_arrive(&it_empty[r & 1]);
+        Item w;
+        if (!decode(lin, w)) break;
+        mbar_wait(q_full, r & 1);
         tc_fence_after();
-        const uint32_t p_base = smem_u32(sP + (t * 2 + (j & 1)) * C::P_BYTES);
-        const uint32_t v_base = smem_u32(sV + (j % NST) * C::KV_BYTES);
+        const int ntA = w.ntA, nt = w.ntB;
+        // Ping-pong: while the softmax warps of one query tile work on S(j),
+        // the tensor core runs the other tile's PV(j) and S(j+1); S_t(j+1) is
+        // issued as soon as tile t's softmax has released S_t(j).
+        auto issue_s = [&](int t, int j) {
+          const int c = (t ? cB : cA) + j;
+          const uint32_t k_base = smem_u32(sK + ((g0 + j) % NST) * C::KV_BYTES);
+          const uint32_t q_base = smem_u32(sQ + t * C::Q_BYTES);
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k)
-          mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
-                  smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
-        mma_commit(&o_done[t * 2 + (j & 1)]);
-      };
-      int kv_seen = -1;
-      auto wait_kv = [&](int j) {
-        if (kv_seen >= j) return;
-        mbar_wait(&kv_full[j % NST], (j / NST) & 1);
-        tc_fence_after();
-        kv_seen = j;
-      };
-      // S is double-buffered per tile: S_t(j+2) goes out as soon as the
-      // softmax of tile t has released S_t(j) (its P(j) is in smem)
-      for (int j = 0; j < 2 && j < nt; ++j) {
-        wait_kv(j);
-        if (j < ntA) issue_s(0, j);
-        issue_s(1, j);
-      }
-      for (int j = 0; j < nt; ++j) {
-        if (j < ntA) {
-          issue_o(0, j);
-          if (j + 2 < ntA) {
-            wait_kv(j + 2);
-            issue_s(0, j + 2);
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint32_t qoff = (k >> 2) * C::QSUB + (k & 3) * 32;
+            const uint32_t koff = (k >> 2) * C::KVSUB + (k & 3) * 32;
+            mma_f16(tmem + C::S_COL + (t * 2 + (c & 1)) * BKV, smem_desc(q_base + qoff),
+                    smem_desc(k_base + koff), id_s, k > 0);
           }
+          mma_commit(&s_full[t * 2 + (c & 1)]);
+        };
+        auto issue_o = [&](int t, int j) {
+          const int c = (t ? cB : cA) + j;
+          mbar_wait(&p_full[t * 2 + (c & 1)], (c >> 1) & 1);
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(sP + (t * 2 + (c & 1)) * C::P_BYTES);
+          const uint32_t v_base = smem_u32(sV + ((g0 + j) % NST) * C::KV_BYTES);
+#pragma unroll
+          for (int k = 0; k < BKV / 16; ++k)
+            mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
+                    smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
+          mma_commit(&o_done[t * 2 + (c & 1)]);
+        };
+        int kv_seen = -1;
+        auto wait_kv = [&](int j) {
+          if (kv_seen >= j) return;
+          const int g = g0 + j;
+          mbar_wait(&kv_full[g % NST], (g / NST) & 1);
+          tc_fence_after();
+          kv_seen = j;
+        };
+        // S is double-buffered per tile: S_t(j+2) goes out as soon as the
+        // softmax of tile t has released S_t(j) (its P(j) is in smem)
+        for (int j = 0; j < 2 && j < nt; ++j) {
+          wait_kv(j);
+          if (j < ntA) issue_s(0, j);
+          issue_s(1, j);
         }
-        issue_o(1, j);
-        if (j + 2 < nt) {
-          wait_kv(j + 2);
-          issue_s(1, j + 2);
+        if (nt <= 2) mma_commit(q_empty);                 // last S of the item issued
+        for (int j = 0; j < nt; ++j) {
+          if (j < ntA) {
+            issue_o(0, j);
+            if (j + 2 < ntA) {
+              wait_kv(j + 2);
+              issue_s(0, j + 2);
+            }
+          }
+          issue_o(1, j);
+          if (j + 2 < nt) {
+            wait_kv(j + 2);
+            issue_s(1, j + 2);
+            if (j + 3 == nt) mma_commit(q_empty);
+          }
+          mma_commit(&kv_empty[(g0 + j) % NST]);
         }
-        mma_commit(&kv_empty[j % NST]);
+        g0 += nt;
+        cA += ntA;
+        cB += nt;
       }
     }
   } else {
@@ -333,20 +385,30 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int t = warp >> 2;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;
-    const int qs = q0 + t * BQ + row;
-    const int ntile = t == 0 ? ntA : ntB;
-    const bool live = qs >= pad && qs < a.seq;
-    const int row_kend = live ? (a.causal ? qs + 1 : a.seq) : pad;   // keys [pad, row_kend)
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const uint32_t s_base = tmem + lane_addr + C::S_COL + t * 2 * BKV;
     const uint32_t o_addr = tmem + lane_addr + C::O_COL + t * HD;
     uint8_t* prow0 = sP + (t * 2) * C::P_BYTES + row * 128;
+    int cb = 0;                                           // this tile's counter at item start
+    for (int r = 0;; ++r) {
+    mbar_wait(&it_full[r & 1], (r >> 1) & 1);
+    const int lin = *reinterpret_cast<volatile int*>(&item_buf[r & 1]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&it_empty[r & 1]);
+    Item w;
+    if (!decode(lin, w)) break;
+    const int pad = w.pad;
+    const int qs = w.q0 + t * BQ + row;
+    const int ntile = t == 0 ? w.ntA : w.ntB;
+    const bool live = qs >= pad && qs < a.seq;
+    const int row_kend = live ? (a.causal ? qs + 1 : a.seq) : pad;   // keys [pad, row_kend)
     float m = -INFINITY, l = 0.f;                         // m in log2 units (scaled)
     for (int j = 0; j < ntile; ++j) {
+      const int c = cb + j;
       const int kt = pad + j * BKV;
       const int nvalid = min(max(row_kend - kt, 0), BKV);
-      mbar_wait(&s_full[t * 2 + (j & 1)], (j >> 1) & 1);
-      const uint32_t s_addr = s_base + (j & 1) * BKV;
+      mbar_wait(&s_full[t * 2 + (c & 1)], (c >> 1) & 1);
+      const uint32_t s_addr = s_base + (c & 1) * BKV;
       tc_fence_after();
       float sv[BKV];
       {
@@ -380,8 +442,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       tmax *= a.scale_log2;                               // scale > 0: max commutes
       // P buffer j & 1 was last read by PV(j-2)
-      uint8_t* prow = prow0 + (j & 1) * C::P_BYTES;
-      if (j >= 2) mbar_wait(&o_done[t * 2 + (j & 1)], ((j - 2) >> 1) & 1);
+      uint8_t* prow = prow0 + (c & 1) * C::P_BYTES;
+      if (c >= 2) mbar_wait(&o_done[t * 2 + (c & 1)], ((c - 2) >> 1) & 1);
       tc_fence_after();
       // tcgen05.ld/st are .sync.aligned: the O rescale is decided per warp
       // (any row whose max grew past the threshold rescales the whole warp;
@@ -389,7 +451,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool need = tmax > m + RESCALE_LOG2 || (m == -INFINITY && tmax != -INFINITY);
       if (__any_sync(0xffffffffu, need && m != -INFINITY)) {
         // the O rows must be final up to PV(j-1) before they are rescaled
-        if (j >= 1) mbar_wait(&o_done[t * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+        if (j >= 1) mbar_wait(&o_done[t * 2 + ((c - 1) & 1)], ((c - 1) >> 1) & 1);
         tc_fence_after();
         const float m_new = fmaxf(m, tmax);
         const float f = (m == -INFINITY) ? 1.f : exp2f(m - m_new);   // -inf row: O is still zero
@@ -458,13 +520,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       l += rs;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
       tc_fence_before();
-      mbar_arrive(&p_full[t * 2 + (j & 1)]);
+      mbar_arrive(&p_full[t * 2 + (c & 1)]);
     }
-    if (ntile > 0) mbar_wait(&o_done[t * 2 + ((ntile - 1) & 1)], ((ntile - 1) >> 1) & 1);
+    const int cl = cb + ntile - 1;
+    if (ntile > 0) mbar_wait(&o_done[t * 2 + (cl & 1)], (cl >> 1) & 1);
     tc_fence_after();
     if (ntile > 0) {                                      // warp-uniform TMEM reads
       const float inv = l > 0.f ? 1.0f / l : 0.f;
-      T* dst = reinterpret_cast<T*>(a.o) + ((long long)a.q_rowbase[b] + qs) * a.ldo + head * HD;
+      T* dst = reinterpret_cast<T*>(a.o) + ((long long)a.q_rowbase[w.b] + qs) * a.ldo + w.head * HD;
 #pragma unroll
       for (int c = 0; c < HD / 32; ++c) {
         uint32_t r[32];
@@ -480,11 +543,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    cb += ntile;
+    }
   }
   __syncthreads();
   if (warp == NSM + 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if (n_work > 0 && threadIdx.x == 0) {
+    // the last CTA out re-arms the counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.ctr + 1, 1) == (int)gridDim.x - 1) {
+      a.ctr[0] = 0;
+      a.ctr[1] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -521,30 +595,74 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   const int npair = (p.seq + 2 * BQ - 1) / (2 * BQ);
   static FaItems items;
   a.nitems = 0;
+  a.ctr = nullptr;
   static const bool no_list = std::getenv("EET_ATTN_GRID") != nullptr;   // A/B switch
-  if (p.h_pads && !no_list && npair <= 64 && p.batch <= 1024 && (long long)p.batch * npair <= MAX_ITEMS) {
-    // cost of a pair = key tiles of its two query tiles (0 when in the padding)
-    static std::vector<std::pair<int, int>> work;
-    work.clear();
-    for (int b = 0; b < p.batch; ++b) {
+  if (p.h_pads && !no_list && npair <= 256 && p.heads <= 256 && p.batch <= 65536) {
+    static std::vector<int> order;
+    order.resize(p.batch);
+    for (int b = 0; b < p.batch; ++b) order[b] = b;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.h_pads[x] < p.h_pads[y]; });
+    long long n = 0;
+    for (int b : order) {
       const int pad = p.h_pads[b];
-      for (int pr = npair - 1; pr >= 0; --pr) {
-        const int q0 = pr * 2 * BQ;
+      int pairs = 0;                                    // non-empty pairs: qhiB > pad
+      for (int pr = npair - 1; pr >= 0; --pr)
+        if (std::min((pr + 1) * 2 * BQ, p.seq) > pad) ++pairs;
+      n += (long long)pairs * p.heads;
+    }
+    if (n <= MAX_ITEMS) {
+      // Greedy dynamic scheduling wants the light items last (short tail);
+      // L2 wants the pairs of a (sequence, head) adjacent (shared K/V). So:
+      // NB cost phases, heaviest first, locality order inside each phase.
+      static const int nb_env = [] {
+        const char* e = std::getenv("EET_ATTN_NB");
+        return e ? atoi(e) : 4;
+      }();
+      int maxc = 1;
+      auto cost = [&](int b, int pr) {
+        const int pad = p.h_pads[b], q0 = pr * 2 * BQ;
         const int qhiA = std::min(q0 + BQ, p.seq), qhiB = std::min(q0 + 2 * BQ, p.seq);
-        if (qhiB <= pad) continue;
         const bool liveA = qhiA > pad && q0 < p.seq;
         const int kA = p.causal ? qhiA : p.seq, kB = p.causal ? qhiB : p.seq;
-        const int cost = (liveA ? (kA - pad + BKV - 1) / BKV : 0) + (kB - pad + BKV - 1) / BKV;
-        work.emplace_back(cost, (b << 6) | pr);
-      }
+        return (liveA ? (kA - pad + BKV - 1) / BKV : 0) + (kB - pad + BKV - 1) / BKV;
+      };
+      for (int b = 0; b < p.batch; ++b)
+        if (p.h_pads[b] < p.seq) maxc = std::max(maxc, cost(b, npair - 1));
+      static std::vector<std::pair<int, uint32_t>> work;
+      work.clear();
+      for (int b : order)
+        for (int h = 0; h < p.heads; ++h)
+          for (int pr = npair - 1; pr >= 0; --pr)
+            if (std::min((pr + 1) * 2 * BQ, p.seq) > p.h_pads[b]) {
+              const int c = cost(b, pr);
+              const int phase = nb_env > 0 ? (int)((long long)(maxc - c) * nb_env / (maxc + 1)) : maxc - c;
+              work.emplace_back(phase, ((uint32_t)b << 16) | ((uint32_t)h << 8) | (uint32_t)pr);
+            }
+      std::stable_sort(work.begin(), work.end(),
+                       [](const std::pair<int, uint32_t>& x, const std::pair<int, uint32_t>& y) {
+                         return x.first < y.first;
+                       });
+      int k = 0;
+      for (const auto& e : work) items.v[k++] = e.second;
+      a.nitems = k;
+      if (k == 0) return;
     }
-    std::stable_sort(work.begin(), work.end(),
-                     [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first > y.first; });
-    for (size_t i = 0; i < work.size(); ++i) items.v[i] = (unsigned short)work[i].second;
-    a.nitems = (int)work.size();
-    if (a.nitems == 0) return;
   }
-  dim3 grid = a.nitems > 0 ? dim3((unsigned)(a.nitems * p.heads), 1, 1) : dim3(npair, p.heads, p.batch);
+  if (a.nitems > 0) {
+    // counters re-armed by the kernel itself; rotating slots keep launches
+    // on different streams apart
+    static int* ctrs = nullptr;
+    static unsigned slot = 0;
+    constexpr int NSLOT = 64;
+    if (!ctrs) {
+      EET_CHECK_CUDA(cudaMalloc(&ctrs, NSLOT * 2 * sizeof(int)));
+      EET_CHECK_CUDA(cudaMemset(ctrs, 0, NSLOT * 2 * sizeof(int)));
+    }
+    a.ctr = ctrs + 2 * (slot++ % NSLOT);
+  }
+  // list: persistent, one CTA per SM (the smem footprint allows one)
+  dim3 grid = a.nitems > 0 ? dim3((unsigned)std::min(a.nitems, device_sm_count()), 1, 1)
+                           : dim3(npair, p.heads, p.batch);
   ProfScope ps(K_ATTN_PREFILL, st, bytes, flops);
   kern<<<grid, THREADS, C::SMEM, st>>>(mq, mk, mv, a, items);
   EET_LAUNCH_CHECK();

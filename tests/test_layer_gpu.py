@@ -79,7 +79,11 @@ def test_encoder_layer_fp32_matches_reference(eet, name):
 @pytest.mark.parametrize("dt", ["bf16", "fp16"])
 @pytest.mark.parametrize("b,h,heads,lengths", [(4, 768, 12, [64, 47, 47, 47]),
                                                 (3, 1024, 8, [200, 17, 129]),
-                                                (2, 2048, 16, [300, 1])])
+                                                (2, 2048, 16, [300, 1]),
+                                                # > 148 attention work items: the
+                                                # persistent CTAs loop over items
+                                                (6, 1024, 16, [900, 700, 1, 513, 256, 880]),
+                                                (4, 2048, 16, [640, 300, 129, 600])])
 def test_decoder_layer_16bit_vs_oracle(eet, dt, b, h, heads, lengths):
     """North-star 16-bit tolerance 2e-2 (combined) vs the fp32 oracle on the
     same fp32 weights; exercises the tcgen05 GEMMs (T > 16 rows) and the
