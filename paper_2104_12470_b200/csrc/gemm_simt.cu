@@ -15,18 +15,24 @@ namespace eet {
 
 // ------------------------------------------------------------- fp32 GEMM
 namespace {
-constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int BM = 128, BN = 128, BK = 8;
 }
 
+// 128x128 tile, 256 threads, 8x8 outputs per thread as 2x2 blocks of 4x4
+// (rows ty*4 and 64+ty*4, columns tx*4 and 64+tx*4: conflict-free float4
+// shared reads, 16 FFMA per 128-bit shared load). A and B k-slices are
+// staged transposed ([k][m], [k][n]) in a double-buffered ring; global
+// loads are 128-bit along k when rows are 16-byte aligned (VEC).
 // split-K: blockIdx.z = split, K range [z * kspan, (z+1) * kspan); with
 // part != nullptr the tile is stored raw to part[z][M][N] (the reduction
 // kernel applies the epilogue), else the epilogue runs here.
-__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, int lda,
-                                                       const float* __restrict__ B, int ldb,
-                                                       int M, int N, int K, Epi e, int kspan,
-                                                       float* __restrict__ part) {
-  __shared__ __align__(16) float As[2][BK][BM + 4];
-  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+template <bool VEC>
+__global__ void __launch_bounds__(256, 2) gemm_f32_kernel(const float* __restrict__ A, int lda,
+                                                          const float* __restrict__ B, int ldb,
+                                                          int M, int N, int K, Epi e, int kspan,
+                                                          float* __restrict__ part) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -34,17 +40,26 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
   A += kbeg;
   B += kbeg;
   K = min(kspan, K - kbeg);
-  // loader mapping: 64 rows x 16 k = 1024 elements; thread -> row lr, k lk..lk+3
-  const int lr = tid >> 2, lk = (tid & 3) * 4;
-  float acc[4][4] = {};
+  // loader: 128 rows x 8 k per operand; thread -> row lr, k lk..lk+3
+  const int lr = tid >> 1, lk = (tid & 1) * 4;
+  const bool a_ok = m0 + lr < M, b_ok = n0 + lr < N;
+  const float* Ap = A + (long long)(a_ok ? m0 + lr : 0) * lda;
+  const float* Bp = B + (long long)(b_ok ? n0 + lr : 0) * ldb;
+  float acc[8][8] = {};
   float ra[4], rb[4];
   auto gload = [&](int k0) {
+    const int k = k0 + lk;
+    if (VEC && k + 3 < K) {
+      const float4 va = a_ok ? __ldg(reinterpret_cast<const float4*>(Ap + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 vb = b_ok ? __ldg(reinterpret_cast<const float4*>(Bp + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      ra[0] = va.x; ra[1] = va.y; ra[2] = va.z; ra[3] = va.w;
+      rb[0] = vb.x; rb[1] = vb.y; rb[2] = vb.z; rb[3] = vb.w;
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int k = k0 + lk + j;
-      int am = m0 + lr, bn = n0 + lr;
-      ra[j] = (am < M && k < K) ? A[(long long)am * lda + k] : 0.f;
-      rb[j] = (bn < N && k < K) ? B[(long long)bn * ldb + k] : 0.f;
+      for (int j = 0; j < 4; ++j) {
+        ra[j] = (a_ok && k + j < K) ? Ap[k + j] : 0.f;
+        rb[j] = (b_ok && k + j < K) ? Bp[k + j] : 0.f;
+      }
     }
   };
   auto sstore = [&](int buf) {
@@ -63,13 +78,16 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
     if (kt + 1 < nk) gload((kt + 1) * BK);
 #pragma unroll
     for (int k = 0; k < BK; ++k) {
-      float4 a = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
-      float4 b = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
-      float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
     if (kt + 1 < nk) {
       sstore(buf ^ 1);
@@ -77,12 +95,12 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
     }
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int m = m0 + ty * 4 + i;
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
     if (m >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int n = n0 + tx * 4 + j;
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
       if (n >= N) continue;
       if (part) part[((size_t)blockIdx.z * M + m) * N + n] = acc[i][j];
       else epi_apply<float>(e, m, n, acc[i][j]);
@@ -101,14 +119,14 @@ __global__ void gemm_f32_reduce_kernel(const float* __restrict__ part, int split
   }
 }
 
-// Split-K plan: ~4 CTAs of 256 threads per SM, >= 128 k per split. The
+// Split-K plan: ~2 CTAs of 256 threads per SM, >= 128 k per split. The
 // partial workspace is device memory grown outside graph capture; under
 // capture (or if it would have to grow) the GEMM runs unsplit.
 void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M, int N, int K,
                    const Epi& e, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
   const int tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
-  int splits = std::max(1, std::min(4 * device_sm_count() / std::max(1, tiles), K / 128));
+  int splits = std::max(1, std::min(2 * device_sm_count() / std::max(1, tiles), K / 128));
   static float* ws = nullptr;
   static size_t ws_bytes = 0;
   if (splits > 1) {
@@ -130,7 +148,12 @@ void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M, int 
   splits = (K + kspan - 1) / kspan;
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, splits);
   ProfScope ps(K_GEMM_F32, st, gemm_bytes(M, N, K, 4, e), 2.0 * M * N * K);
-  gemm_f32_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, splits > 1 ? ws : nullptr);
+  const bool vec = lda % 4 == 0 && ldb % 4 == 0 && kspan % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+  if (vec)
+    gemm_f32_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, splits > 1 ? ws : nullptr);
+  else
+    gemm_f32_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, splits > 1 ? ws : nullptr);
   EET_LAUNCH_CHECK();
   if (splits > 1) {
     const long long total = (long long)M * N;

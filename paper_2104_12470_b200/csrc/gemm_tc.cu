@@ -20,6 +20,8 @@
 // Row tails and K tails are handled by TMA zero fill (OOB) + epilogue guards.
 #include "sm100.cuh"
 
+#include <cstdlib>
+
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -88,8 +90,8 @@ template <int BN> struct Cfg {
 // A panel (GM*128 rows, kept in L2) and a few B column blocks. The plain
 // M-fastest order re-streamed all of A from HBM for every N-tile (c4 QKV:
 // 13.3 GB of DRAM reads per launch for 1.2 GB of operands).
-constexpr int GM = 32;
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+// GM is chosen on the host so that the A panel fits well inside L2.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int GM, int& mb, int& nb) {
   const int panel = GM * num_n;
   const int p = tile / panel;
   const int m0 = p * GM;
@@ -99,10 +101,15 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int&
   mb = m0 + r % gm;
 }
 
+struct L2Plan {
+  int gm;                  // M-tiles per raster group
+  uint64_t pol_a, pol_b;   // L2 cache policies of the A / B TMA loads
+};
+
 template <typename T, int BN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA,
-                   const __grid_constant__ CUtensorMap mapB, int M, int N, int K, Epi e) {
+                   const __grid_constant__ CUtensorMap mapB, int M, int N, int K, Epi e, L2Plan L) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -146,15 +153,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // activations are streamed once per N-tile; weights are re-read by
-      // every M-tile of the column block -> keep weights in L2
-      const uint64_t pol_first = 0x12F0000000000000ull;  // EVICT_FIRST
-      const uint64_t pol_last = 0x14F0000000000000ull;   // EVICT_LAST
+      // the A panel is re-read by every N-tile of its group (kept in L2);
+      // a B block is re-read only by the group's M-tiles running next to it
+      const uint64_t pol_first = L.pol_a;
+      const uint64_t pol_last = L.pol_b;
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
         int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
+        tile_coords(tile, num_m, num_n, L.gm, mb, nb);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int local = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++local) {
       int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords(tile, num_m, num_n, L.gm, mb, nb);
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
@@ -251,8 +258,27 @@ static void launch(const void* A, int lda, const void* B, int ldb, int M, int N,
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = std::min(tiles, device_sm_count());
+  // A panel of GM M-tiles <= ~40 MB (a third of L2), GM in [4, 32]
+  static const int mode = [] {
+    const char* v = std::getenv("EET_GEMM_L2");
+    return v ? atoi(v) : 1;
+  }();
+  constexpr uint64_t EVICT_NORMAL = 0x1000000000000000ull, EVICT_FIRST = 0x12F0000000000000ull,
+                     EVICT_LAST = 0x14F0000000000000ull;
+  L2Plan L;
+  const long long panel_row_bytes = (long long)BM * K * 2;
+  L.gm = (int)std::max(4LL, std::min(32LL, (40LL << 20) / std::max(1LL, panel_row_bytes)));
+  L.pol_a = EVICT_LAST;
+  L.pol_b = EVICT_NORMAL;
+  if (mode == 0) {                       // previous plan: GM 32, A evict-first, B evict-last
+    L.gm = 32;
+    L.pol_a = EVICT_FIRST;
+    L.pol_b = EVICT_LAST;
+  } else if (mode == 2) {
+    L.pol_a = EVICT_NORMAL;
+  }
   ProfScope ps(K_GEMM_TC, st, gemm_bytes(M, N, K, 2, e), 2.0 * M * N * K);
-  kern<<<grid, THREADS, C::SMEM, st>>>(ma, mb, M, N, K, e);
+  kern<<<grid, THREADS, C::SMEM, st>>>(ma, mb, M, N, K, e, L);
   EET_LAUNCH_CHECK();
 }
 
