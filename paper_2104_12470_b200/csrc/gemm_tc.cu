@@ -259,6 +259,7 @@ static void launch(const void* A, int lda, const void* B, int ldb, int M, int N,
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = std::min(tiles, device_sm_count());
   // A panel of GM M-tiles <= ~40 MB (a third of L2), GM in [4, 32]
+  // (panel budget sweep, tools/gpu_gemm_panel.sh: 20-96 MB within 1% on c3/c4)
   static const int mode = [] {
     const char* v = std::getenv("EET_GEMM_L2");
     return v ? atoi(v) : 1;
@@ -267,7 +268,14 @@ static void launch(const void* A, int lda, const void* B, int ldb, int M, int N,
                      EVICT_LAST = 0x14F0000000000000ull;
   L2Plan L;
   const long long panel_row_bytes = (long long)BM * K * 2;
-  L.gm = (int)std::max(4LL, std::min(32LL, (40LL << 20) / std::max(1LL, panel_row_bytes)));
+  static const long long panel_mb = [] {
+    const char* v = std::getenv("EET_GEMM_PANEL_MB");
+    return v ? atoll(v) : 40LL;
+  }();
+  L.gm = (int)std::max(4LL, std::min(32LL, (panel_mb << 20) / std::max(1LL, panel_row_bytes)));
+  // all of A within ~96 MB: one group, B streamed exactly once (c5: -4%)
+  const int num_m = (M + BM - 1) / BM;
+  if (num_m <= 32 && (long long)num_m * panel_row_bytes <= (96LL << 20)) L.gm = num_m;
   L.pol_a = EVICT_LAST;
   L.pol_b = EVICT_NORMAL;
   if (mode == 0) {                       // previous plan: GM 32, A evict-first, B evict-last
