@@ -580,6 +580,11 @@ int decode_splits(int batch, int heads, int smax, int hd, int es) {
   const int slots = 3 * device_sm_count();
   const int by_sms = std::max(1, slots / pairs);
   const int cap = std::max(1, (smax + 63) / 64);       // >= 64 keys per split
+  static const int forced = [] {                       // A/B switch
+    const char* e = std::getenv("EET_DEC_SPLITS");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) return std::min(forced, cap);
   return std::max(1, std::min(by_sms, std::min(cap, 64)));
 }
 
@@ -647,7 +652,15 @@ static void decode_dispatch(const DecodeArgs& a, cudaStream_t st) {
         const char* e = std::getenv("EET_ATTN_E8");
         return (e && e[0] == '1') ? 0 : 1;
       }();
-      if (sizeof(T) == 2 && hd == 64 && e16) return decode_bulk_launch<T, 2 * VE, 4>(a, st);
+      static const int nbuf = [] {                     // A/B switch: ring depth
+        const char* e = std::getenv("EET_DEC_NBUF");
+        return e ? atoi(e) : 4;
+      }();
+      if (sizeof(T) == 2 && hd == 64 && e16) {
+        if (nbuf == 3) return decode_bulk_launch_n<T, 2 * VE, 4, 3>(a, st);
+        if (nbuf == 2) return decode_bulk_launch_n<T, 2 * VE, 4, 2>(a, st);
+        return decode_bulk_launch<T, 2 * VE, 4>(a, st);
+      }
       if (lanes <= 1) return decode_bulk_launch<T, VE, 1>(a, st);
       if (lanes <= 2) return decode_bulk_launch<T, VE, 2>(a, st);
       if (lanes <= 4) return decode_bulk_launch<T, VE, 4>(a, st);

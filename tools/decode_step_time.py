@@ -25,9 +25,10 @@ def main():
             a.record(); eet.generate(w, req, cfg, pool=pool); e.record(); torch.cuda.synchronize()
             ts.append(a.elapsed_time(e))
         return statistics.median(ts)
-    t1, t2 = run(8), run(136)
-    tag = " ".join(f"{k}={os.environ[k]}" for k in ("EET_NO_PACKED", "EET_ATTN_RANGE", "EET_MEGAKERNEL") if k in os.environ)
-    print(f"b{b} L{layers} [{tag}] prompt+8: {t1:.2f} ms  per decode step: {(t2 - t1) / 128 * 1e3:.1f} us", flush=True)
+    s2 = int(os.environ.get("STEPS2", "136"))
+    t1, t2 = run(8), run(s2)
+    tag = " ".join(f"{k}={os.environ[k]}" for k in ("EET_NO_PACKED", "EET_MEGAKERNEL", "EET_DEC_SPLITS", "EET_DEC_NBUF") if k in os.environ)
+    print(f"b{b} L{layers} [{tag}] prompt+8: {t1:.2f} ms  per decode step (8..{s2}): {(t2 - t1) / (s2 - 8) * 1e3:.1f} us", flush=True)
 
 if __name__ == "__main__":
     main()

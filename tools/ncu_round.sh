@@ -24,3 +24,8 @@ timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c3 -f python too
 timeout 600 $NCU $FULL -k regex:gemm_tc -s 4 -c 4 -o $O/gemm_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/gemm_tc_c4.log 2>&1
 timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/attn_tc_c4.log 2>&1
 ls -la $O
+# summaries on the box; the .ncu-rep files are too large to bring back
+for r in $O/*.ncu-rep; do python tools/ncu_summary.py full $r > ${r%.ncu-rep}.full.txt 2>&1; done
+for w in c2 c3 c4 c5; do python tools/ncu_summary.py launches $O/launches_$w.csv > $O/launches_$w.txt 2>&1; done
+rm -f $O/*.ncu-rep
+gzip -f $O/launches_c2.csv
