@@ -15,10 +15,10 @@ namespace eet {
 
 // ------------------------------------------------------------- fp32 GEMM
 namespace {
-constexpr int BM = 128, BN = 128, BK = 8;
+constexpr int BM = 128, BN = 128, BK = 16;
 }
 
-// 128x128 tile, 256 threads, 8x8 outputs per thread as 2x2 blocks of 4x4
+// 128x128x16 tile, 256 threads, 8x8 outputs per thread as 2x2 blocks of 4x4
 // (rows ty*4 and 64+ty*4, columns tx*4 and 64+tx*4: conflict-free float4
 // shared reads, 16 FFMA per 128-bit shared load). A and B k-slices are
 // staged transposed ([k][m], [k][n]) in a double-buffered ring; global
@@ -40,33 +40,48 @@ __global__ void __launch_bounds__(256, 2) gemm_f32_kernel(const float* __restric
   A += kbeg;
   B += kbeg;
   K = min(kspan, K - kbeg);
-  // loader: 128 rows x 8 k per operand; thread -> row lr, k lk..lk+3
-  const int lr = tid >> 1, lk = (tid & 1) * 4;
-  const bool a_ok = m0 + lr < M, b_ok = n0 + lr < N;
-  const float* Ap = A + (long long)(a_ok ? m0 + lr : 0) * lda;
-  const float* Bp = B + (long long)(b_ok ? n0 + lr : 0) * ldb;
+  // loader: 128 rows x 16 k per operand; thread -> rows lr and lr + 64,
+  // k lk..lk+3 (two float4 per operand per slice)
+  const int lr = tid >> 2, lk = (tid & 3) * 4;
+  bool a_ok[2], b_ok[2];
+  const float* Ap[2];
+  const float* Bp[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    a_ok[h] = m0 + lr + 64 * h < M;
+    b_ok[h] = n0 + lr + 64 * h < N;
+    Ap[h] = A + (long long)(a_ok[h] ? m0 + lr + 64 * h : 0) * lda;
+    Bp[h] = B + (long long)(b_ok[h] ? n0 + lr + 64 * h : 0) * ldb;
+  }
   float acc[8][8] = {};
-  float ra[4], rb[4];
+  float4 ra[2], rb[2];
   auto gload = [&](int k0) {
     const int k = k0 + lk;
-    if (VEC && k + 3 < K) {
-      const float4 va = a_ok ? __ldg(reinterpret_cast<const float4*>(Ap + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 vb = b_ok ? __ldg(reinterpret_cast<const float4*>(Bp + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      ra[0] = va.x; ra[1] = va.y; ra[2] = va.z; ra[3] = va.w;
-      rb[0] = vb.x; rb[1] = vb.y; rb[2] = vb.z; rb[3] = vb.w;
-    } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        ra[j] = (a_ok && k + j < K) ? Ap[k + j] : 0.f;
-        rb[j] = (b_ok && k + j < K) ? Bp[k + j] : 0.f;
+    for (int h = 0; h < 2; ++h) {
+      if (VEC && k + 3 < K) {
+        ra[h] = a_ok[h] ? __ldg(reinterpret_cast<const float4*>(Ap[h] + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        rb[h] = b_ok[h] ? __ldg(reinterpret_cast<const float4*>(Bp[h] + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        float va[4], vb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          va[j] = (a_ok[h] && k + j < K) ? Ap[h][k + j] : 0.f;
+          vb[j] = (b_ok[h] && k + j < K) ? Bp[h][k + j] : 0.f;
+        }
+        ra[h] = make_float4(va[0], va[1], va[2], va[3]);
+        rb[h] = make_float4(vb[0], vb[1], vb[2], vb[3]);
       }
     }
   };
   auto sstore = [&](int buf) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      As[buf][lk + j][lr] = ra[j];
-      Bs[buf][lk + j][lr] = rb[j];
+    for (int h = 0; h < 2; ++h) {
+      const int r = lr + 64 * h;
+      As[buf][lk + 0][r] = ra[h].x; As[buf][lk + 1][r] = ra[h].y;
+      As[buf][lk + 2][r] = ra[h].z; As[buf][lk + 3][r] = ra[h].w;
+      Bs[buf][lk + 0][r] = rb[h].x; Bs[buf][lk + 1][r] = rb[h].y;
+      Bs[buf][lk + 2][r] = rb[h].z; Bs[buf][lk + 3][r] = rb[h].w;
     }
   };
   const int nk = (K + BK - 1) / BK;
