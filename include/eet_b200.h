@@ -134,6 +134,12 @@ int eet_mha_forward(const float* q, const float* k, const float* v, float* out,
 int eet_gemm(int dtype, const void* A, const void* B, const float* bias,
              float* C, int M, int N, int K, int ldc, void* stream);
 
+/* Weight packing on the device: dst[c][r] = (dtype) src[r][c] for a
+ * row-major float32 src [rows, cols]. Turns the reference's [in, out]
+ * matrices (weights.py:31-51; MFW1 payload, weights.py:142-204) into the
+ * K-major [out, in] compute layout without a host-side transpose. */
+int eet_transpose_cast(int dtype, const float* src, int rows, int cols, void* dst, void* stream);
+
 /* Decode GEMV through the packed-fragment path (gemv_mma.cu): packs W
  * [N, K] (K-major, 16-bit) and computes out[M, N] = X[M, K] W^T in fp32,
  * M <= 16. repack = 0 reuses the copy packed by an earlier call for the same

@@ -59,6 +59,7 @@ SIGNATURES = {
     "eet_profile_kind_name": (C.c_char_p, [i32]),
     "eet_set_decode_megakernel": (i32, [i32]),
     "eet_gemv_packed": (i32, [i32, p, i32, i32, p, i32, p, i32, p]),
+    "eet_transpose_cast": (i32, [i32, p, i32, i32, p, p]),
     "eet_debug_launch_chain": (i32, [i32, i32, i32, p, p]),
     "eet_debug_ktrace": (i32, [i32, p, p]),
     "eet_profile_summary": (i32, [i32, C.POINTER(u64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -510,6 +510,52 @@ __global__ void empty_link_kernel(int* p) {
   if (p && threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(p, 1);
 }
 
+// ------------------------------------------------------- weight packing
+// dst[c][r] = cast(src[r][c]): the reference's [in, out] float32 matrices
+// (weights.py:31-51, MFW1 payload order) become the kernels' K-major
+// [out, in] layout in the compute dtype, on the device, in one pass
+// through a 32x33 shared tile (coalesced reads and writes).
+template <typename T>
+__global__ void transpose_cast_kernel(const float* __restrict__ src, int rows, int cols,
+                                      T* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[(size_t)r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) dst[(size_t)c * rows + r] = from_f<T>(tile[threadIdx.x][i]);
+  }
+}
+
+extern "C" int eet_transpose_cast(int dtype, const float* src, int rows, int cols, void* dst,
+                                  void* stream) {
+  try {
+    EET_REQUIRE(src && dst, EET_ERR_ARG, "transpose_cast: null pointer");
+    EET_REQUIRE(rows >= 0 && cols >= 0, EET_ERR_SHAPE, "transpose_cast: negative extent");
+    if (rows == 0 || cols == 0) return EET_OK;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+    EET_REQUIRE(grid.y <= 65535u, EET_ERR_SHAPE, "transpose_cast: too many rows");
+    if (dtype == EET_F32)
+      transpose_cast_kernel<float><<<grid, block, 0, st>>>(src, rows, cols, static_cast<float*>(dst));
+    else if (dtype == EET_BF16)
+      transpose_cast_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(src, rows, cols, static_cast<__nv_bfloat16*>(dst));
+    else if (dtype == EET_F16)
+      transpose_cast_kernel<__half><<<grid, block, 0, st>>>(src, rows, cols, static_cast<__half*>(dst));
+    else
+      EET_REQUIRE(false, EET_ERR_ARG, "transpose_cast: unknown dtype");
+    count_launch();
+    EET_LAUNCH_CHECK();
+    return EET_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+
 }  // namespace eet
 
 extern "C" int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream) {

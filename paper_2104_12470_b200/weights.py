@@ -149,10 +149,86 @@ def load_weights(path) -> ModelWeights:
                         arrays[-3], arrays[-2], arrays[-1])
 
 
+def load_weights_device(path) -> ModelWeights:
+    """MFW1 blob straight to the device (same validation as
+    ``load_weights``): the payload is read into pinned host memory, copied to
+    HBM in one transfer, and the returned ``ModelWeights`` holds float32 CUDA
+    views of it. ``DeviceLayer`` / ``DeviceModel`` then build the K-major
+    compute layout with the native transpose+cast kernel
+    (``eet_transpose_cast``) -- no host-side transposes or per-array copies."""
+    import torch
+    with open(path, "rb") as fh:
+        head = fh.read(4 + _HEADER.size)
+        if head[:4] != MAGIC:
+            raise ValueError(f"bad magic {head[:4]!r}, expected {MAGIC!r}")
+        if len(head) < 4 + _HEADER.size:
+            raise ValueError("weight blob truncated")
+        version, h, nl, heads, vocab, max_seq = _HEADER.unpack(head[4:])
+        if version != VERSION:
+            raise ValueError(f"unsupported blob version {version}")
+        shapes = [(vocab, h), (max_seq, h)] + _layer_shapes(h) * nl + [(h,), (h,), (h, vocab)]
+        need = sum(int(np.prod(s)) for s in shapes)
+        fh.seek(0, 2)
+        have = (fh.tell() - 4 - _HEADER.size)
+        if have % 4:
+            raise ValueError("weight blob length is not a whole number of floats")
+        have //= 4
+        if have < need:
+            raise ValueError("weight blob truncated")
+        if have > need:
+            raise ValueError(f"{have - need} trailing floats in weight blob")
+        host = torch.empty(need, dtype=torch.float32, pin_memory=True)
+        fh.seek(4 + _HEADER.size)
+        fh.readinto(host.numpy().view(np.uint8))
+    dev = host.to("cuda", non_blocking=True)
+    torch.cuda.current_stream().synchronize()          # host staging buffer is released below
+    del host
+    arrays, off = [], 0
+    for s in shapes:
+        n = int(np.prod(s))
+        arrays.append(dev[off:off + n].view(*s))
+        off += n
+    layers = [LayerWeights(*arrays[2 + 10 * i: 12 + 10 * i]) for i in range(nl)]
+    return ModelWeights(h, heads, vocab, max_seq, arrays[0], arrays[1], layers,
+                        arrays[-3], arrays[-2], arrays[-1])
+
+
 # ------------------------------------------------------------------ device
+def _is_dev(a) -> bool:
+    try:
+        import torch
+    except ImportError:                                    # pragma: no cover
+        return False
+    return isinstance(a, torch.Tensor) and a.is_cuda
+
+
 def _dev(a, dtype):
     import torch
+    if _is_dev(a):
+        return a.to(dtype=dtype).contiguous()
     return torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32)).to(device="cuda", dtype=dtype).contiguous()
+
+
+def _dev_t(mats, dtype_code: int, td):
+    """Row-stack of the transposes of ``mats`` (each [in, out]) in the
+    compute dtype: [sum(out), in]. Device-resident float32 inputs go through
+    the native transpose+cast kernel; host arrays through numpy."""
+    import torch
+    if all(_is_dev(m) for m in mats):
+        rows = mats[0].shape[0]
+        if any(m.shape[0] != rows for m in mats):
+            raise ValueError("stacked matrices need the same input width")
+        out = torch.empty((sum(int(m.shape[1]) for m in mats), rows), dtype=td, device="cuda")
+        r0 = 0
+        for m in mats:
+            m = m.to(torch.float32).contiguous()
+            cols = int(m.shape[1])
+            _lib.call("eet_transpose_cast", dtype_code, m.data_ptr(), rows, cols, out[r0:r0 + cols].data_ptr(),
+                      torch.cuda.current_stream().cuda_stream)
+            r0 += cols
+        return out
+    host = mats[0] if len(mats) == 1 else np.concatenate([np.asarray(m) for m in mats], axis=1)
+    return _dev(np.asarray(host).T, td)
 
 
 def _ptr(t) -> int | None:
@@ -170,11 +246,10 @@ class DeviceLayer:
         self.dtype = dtype_code
         self.ln1_g, self.ln1_b = _dev(w.ln1_scale, f32), _dev(w.ln1_shift, f32)
         self.ln2_g, self.ln2_b = _dev(w.ln2_scale, f32), _dev(w.ln2_shift, f32)
-        qkv = np.concatenate([np.asarray(w.wq), np.asarray(w.wk), np.asarray(w.wv)], axis=1)
-        self.wqkv = _dev(qkv.T, td)                 # [3h, h]
-        self.wo = _dev(np.asarray(w.wo).T, td)      # [h, h]
-        self.w1 = _dev(np.asarray(w.w1).T, td)      # [4h, h]
-        self.w2 = _dev(np.asarray(w.w2).T, td)      # [h, 4h]
+        self.wqkv = _dev_t([w.wq, w.wk, w.wv], dtype_code, td)   # [3h, h]
+        self.wo = _dev_t([w.wo], dtype_code, td)                   # [h, h]
+        self.w1 = _dev_t([w.w1], dtype_code, td)                   # [4h, h]
+        self.w2 = _dev_t([w.w2], dtype_code, td)                   # [h, 4h]
         b = biases or {}
         self.b_qkv = _dev(b["qkv"], f32) if "qkv" in b else None
         self.b_o = _dev(b["o"], f32) if "o" in b else None
@@ -208,7 +283,7 @@ class DeviceModel:
         self.pos = _dev(w.position_embedding, td)
         self.lnf_g = _dev(w.final_scale, torch.float32)
         self.lnf_b = _dev(w.final_shift, torch.float32)
-        self.head = _dev(np.asarray(w.output_head).T, td)    # [vocab, h]
+        self.head = _dev_t([w.output_head], dtype_code, td)  # [vocab, h]
         self.vocab = w.vocab
         self.max_sequence = w.max_sequence
         arr = _lib.LayerWeightsC * max(1, len(self.layers))
