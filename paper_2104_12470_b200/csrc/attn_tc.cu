@@ -22,6 +22,7 @@
 
 #include <cstdlib>
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 namespace eet {
@@ -593,12 +594,12 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
     attr = true;
   }
   const int npair = (p.seq + 2 * BQ - 1) / (2 * BQ);
-  static FaItems items;
+  thread_local FaItems items;         // copied into the launch parameters
   a.nitems = 0;
   a.ctr = nullptr;
   static const bool no_list = std::getenv("EET_ATTN_GRID") != nullptr;   // A/B switch
   if (p.h_pads && !no_list && npair <= 256 && p.heads <= 256 && p.batch <= 65536) {
-    static std::vector<int> order;
+    thread_local std::vector<int> order;
     order.resize(p.batch);
     for (int b = 0; b < p.batch; ++b) order[b] = b;
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.h_pads[x] < p.h_pads[y]; });
@@ -628,7 +629,7 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
       };
       for (int b = 0; b < p.batch; ++b)
         if (p.h_pads[b] < p.seq) maxc = std::max(maxc, cost(b, npair - 1));
-      static std::vector<std::pair<int, uint32_t>> work;
+      thread_local std::vector<std::pair<int, uint32_t>> work;
       work.clear();
       for (int b : order)
         for (int h = 0; h < p.heads; ++h)
@@ -651,14 +652,15 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   if (a.nitems > 0) {
     // counters re-armed by the kernel itself; rotating slots keep launches
     // on different streams apart
-    static int* ctrs = nullptr;
-    static unsigned slot = 0;
     constexpr int NSLOT = 64;
-    if (!ctrs) {
-      EET_CHECK_CUDA(cudaMalloc(&ctrs, NSLOT * 2 * sizeof(int)));
-      EET_CHECK_CUDA(cudaMemset(ctrs, 0, NSLOT * 2 * sizeof(int)));
-    }
-    a.ctr = ctrs + 2 * (slot++ % NSLOT);
+    static int* const ctrs = [] {                     // thread-safe one-time init
+      int* c = nullptr;
+      EET_CHECK_CUDA(cudaMalloc(&c, NSLOT * 2 * sizeof(int)));
+      EET_CHECK_CUDA(cudaMemset(c, 0, NSLOT * 2 * sizeof(int)));
+      return c;
+    }();
+    static std::atomic<unsigned> slot{0};
+    a.ctr = ctrs + 2 * (slot.fetch_add(1, std::memory_order_relaxed) % NSLOT);
   }
   // list: persistent, one CTA per SM (the smem footprint allows one)
   dim3 grid = a.nitems > 0 ? dim3((unsigned)std::min(a.nitems, device_sm_count()), 1, 1)
