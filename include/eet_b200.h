@@ -100,6 +100,12 @@ int eet_pool_ledger_size(eet_pool* pool, size_t* n);
 /* buffer i in creation order: capacity (bytes) and whether it is idle */
 int eet_pool_buffer_count(eet_pool* pool, size_t* n);
 int eet_pool_buffer_info(eet_pool* pool, size_t i, uint64_t* capacity, int* idle);
+/* Debug poisoning: fill every idle buffer with the byte `value` (0xFF makes
+ * every fp32 / fp16 / bf16 element a NaN), synchronously. A later request
+ * that reuses the buffer sees the pattern, so a kernel that reads scratch it
+ * never wrote shows up as non-finite output. No reference counterpart
+ * (the reference's numpy buffers come zeroed or written). */
+int eet_pool_debug_fill(eet_pool* pool, int value);
 /* event: 0 request, 1 release; decision: 0 malloc, 1 reuse, 2 idle */
 int eet_pool_ledger_get(eet_pool* pool, size_t i, int* event, uint64_t* bytes,
                         int* decision, char* tag, size_t tag_cap);

@@ -29,6 +29,7 @@ __all__ = [
     "window_bounds", "masked_softmax", "step_softmax", "mha",
     "OracleKV", "decoder_layer", "encoder_layer", "generate",
     "seeded_weights", "OracleLayer", "OracleModel", "head_logits",
+    "decoder_layer_rows",
 ]
 
 
@@ -292,6 +293,37 @@ def decoder_layer(x, w, kv: OracleKV, pads, layer: int, heads: int):
     return _ffn(x, w)
 
 
+def decoder_layer_rows(x, w, pads, heads: int, rows, kv: OracleKV | None = None, layer: int = 0):
+    """Prompt-phase decoder layer (empty cache) evaluated at the query slots
+    ``rows`` only: [b, len(rows), h]. Same arithmetic as ``decoder_layer``
+    (runtime.py:106-214): K/V come from every slot, but the score plane,
+    out-projection and FFN are formed for the selected queries alone, which
+    keeps the s=4096 / h=12288 layer shapes within seconds on the host.
+    Rows inside a sequence's padding come out as whatever the reference
+    computes there (pad-query attention rows are exact zeros,
+    attention.py:97-101) and are not compared. With ``kv`` the prompt's K/V
+    are written into it (slots [0, t), memory.py:277-292) so incremental
+    steps can follow."""
+    x = np.asarray(x, dtype=F32)
+    b, t, h = x.shape
+    hd = h // heads
+    rows = np.asarray(rows, dtype=np.int64)
+    ln1 = layer_norm(x, w.ln1_scale, w.ln1_shift)
+    k = (ln1 @ w.wk).reshape(b, t, heads, hd).transpose(0, 2, 1, 3)
+    v = (ln1 @ w.wv).reshape(b, t, heads, hd).transpose(0, 2, 1, 3)
+    if kv is not None:
+        kv.write(layer, 0, k.transpose(0, 2, 1, 3).reshape(b, t, h), v.transpose(0, 2, 1, 3).reshape(b, t, h))
+    q = (ln1[:, rows] @ w.wq).reshape(b, len(rows), heads, hd).transpose(0, 2, 1, 3)
+    sc = np.matmul(q, k.transpose(0, 1, 3, 2)) * F32(1.0 / math.sqrt(hd))   # [b, n, r, t]
+    p = np.empty_like(sc)
+    for i, pad in enumerate(pads):
+        win = window_bounds(pad, t, True)[rows]                             # [r, t]
+        p[i] = _softmax_in_window(sc[i], win[None])
+    ctx = np.matmul(p, v).transpose(0, 2, 1, 3).reshape(b, len(rows), h)
+    xr = x[:, rows] + ctx @ w.wo
+    return _ffn(xr, w)
+
+
 def encoder_layer(x, w, pads, heads: int):
     """Bidirectional pre-norm layer (runtime.py:266-301)."""
     x = np.asarray(x, dtype=F32)
@@ -308,12 +340,18 @@ def head_logits(model, hid):
 
 
 def generate(model, prompts, steps: int, max_sequence: int | None = None,
-             collect_logits: bool = False, layer_limit: int | None = None):
+             collect_logits: bool = False, layer_limit: int | None = None,
+             forced=None):
     """Greedy two-phase generation (runtime.py:372-437). Returns
     (tokens int64 [b, steps], list of per-step logits if requested).
 
     ``layer_limit`` runs only the first N layers (used by the bounded CPU
-    baseline sample; the full path uses every layer)."""
+    baseline sample; the full path uses every layer). ``forced`` (int
+    [b, steps]) teacher-forces the fed-back tokens: step s feeds
+    ``forced[:, s]`` instead of the argmax, so per-step logits of another
+    implementation can be compared with the reference's at every step even
+    after a near-tie picked a different token; the returned tokens are still
+    the reference's own argmax."""
     layers = model.layers if layer_limit is None else model.layers[:layer_limit]
     b = len(prompts)
     pads = left_pads([len(p) for p in prompts])
@@ -337,6 +375,8 @@ def generate(model, prompts, steps: int, max_sequence: int | None = None,
             logs.append(logits.copy())
         nxt = np.argmax(logits, axis=1)                          # lowest id on ties
         toks[:, s] = nxt
+        if forced is not None:
+            nxt = np.asarray(forced, dtype=np.int64)[:, s]
         pos = (t + s) - np.asarray(pads)                         # runtime.py:326-338
         x1 = (model.token_embedding[nxt] + model.position_embedding[pos])[:, None, :]
         for li, w in enumerate(layers):

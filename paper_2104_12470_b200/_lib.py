@@ -71,6 +71,7 @@ SIGNATURES = {
     "eet_pool_release": (i32, [p, i32, sz]),
     "eet_pool_stats": (i32, [p, C.POINTER(u64)]),
     "eet_pool_ledger_size": (i32, [p, C.POINTER(sz)]),
+    "eet_pool_debug_fill": (i32, [p, i32]),
     "eet_pool_buffer_count": (i32, [p, C.POINTER(sz)]),
     "eet_pool_buffer_info": (i32, [p, sz, C.POINTER(u64), C.POINTER(i32)]),
     "eet_pool_ledger_get": (i32, [p, sz, C.POINTER(i32), C.POINTER(u64), C.POINTER(i32), C.c_char_p, sz]),

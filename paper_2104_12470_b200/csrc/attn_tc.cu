@@ -288,15 +288,18 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int s = 0; s < C::KSUB; ++s)
             tma_load_2d(sQ + t * C::Q_BYTES + s * C::QSUB, &mapQ, q_full, w.head * HD + 64 * s,
                         a.q_rowbase[w.b] + w.q0 + t * BQ, pol);
-        const int kv_row0 = (w.b * a.heads + w.head) * a.smax;   // cache row of slot 0
+        // K/V maps are 3-D [b * heads][seq][hd]: the last tile's slots at or
+        // past seq (never written by this pass) arrive as zeros, so masked
+        // keys carry P = 0 against finite V (no 0 * NaN from stale cache)
+        const int plane = w.b * a.heads + w.head;
         for (int j = 0; j < w.ntB; ++j, ++g) {
           const int st = g % NST;
           mbar_wait(&kv_empty[st], ((g / NST) & 1) ^ 1);
           mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
-          const int row = kv_row0 + w.pad + j * BKV;
+          const int slot = w.pad + j * BKV;
           for (int s = 0; s < C::KSUB; ++s) {
-            tma_load_2d(sK + st * C::KV_BYTES + s * C::KVSUB, &mapK, &kv_full[st], 64 * s, row, pol);
-            tma_load_2d(sV + st * C::KV_BYTES + s * C::KVSUB, &mapV, &kv_full[st], 64 * s, row, pol);
+            tma_load_3d(sK + st * C::KV_BYTES + s * C::KVSUB, &mapK, &kv_full[st], 64 * s, slot, plane, pol);
+            tma_load_3d(sV + st * C::KV_BYTES + s * C::KVSUB, &mapV, &kv_full[st], 64 * s, slot, plane, pol);
           }
         }
       }
@@ -568,9 +571,9 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   using C = Cfg<HD>;
   const int h_ld = p.ldq;
   CUtensorMap mq = make_tma_map_2d(p.q, T_rows, h_ld, h_ld, BQ, p.dtype);
-  const int kv_rows = p.batch * p.heads * (int)(p.k_sh / p.hd);        // b * heads * smax
-  CUtensorMap mk = make_tma_map_2d(p.k, kv_rows, HD, HD, BKV, p.dtype);
-  CUtensorMap mv = make_tma_map_2d(p.v, kv_rows, HD, HD, BKV, p.dtype);
+  // K/V window of plane (b, head): slots [0, seq) of its s_max rows
+  CUtensorMap mk = make_tma_map_3d(p.k, p.batch * p.heads, p.seq, HD, p.k_sh, BKV, p.dtype);
+  CUtensorMap mv = make_tma_map_3d(p.v, p.batch * p.heads, p.seq, HD, p.k_sh, BKV, p.dtype);
   FaArgs a;
   a.pads = p.pads;
   a.q_rowbase = p.q_rowbase;
@@ -677,7 +680,7 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
 bool attn_prefill_tc(const PrefillArgs& p, int T_rows, cudaStream_t st, double bytes, double flops) {
   if (p.dtype == EET_F32 || !p.q_rowbase || p.zero_pad_rows) return false;
   if (!(p.hd == 64 || p.hd == 128)) return false;
-  if (p.k_ss != p.hd || p.k_sh % p.hd != 0 || p.ldq % 8 != 0) return false;
+  if (p.k_ss != p.hd || p.k_sh % p.hd != 0 || p.k_sb != p.heads * p.k_sh || p.ldq % 8 != 0) return false;
   if (p.dtype == EET_BF16) {
     p.hd == 64 ? fa::launch<__nv_bfloat16, 64>(p, T_rows, st, bytes, flops)
                : fa::launch<__nv_bfloat16, 128>(p, T_rows, st, bytes, flops);

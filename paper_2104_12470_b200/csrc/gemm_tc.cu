@@ -61,6 +61,26 @@ CUtensorMap make_tma_map_2d(const void* ptr, int rows, int K, int ld, int box_ro
   return map;
 }
 
+// 3-D map over [planes][rows][K] with a plane pitch of plane_ld elements: a
+// box that runs past `rows` inside a plane is zero-filled instead of reading
+// the plane's tail (or the next plane).
+CUtensorMap make_tma_map_3d(const void* ptr, int planes, int rows, int K, long long plane_ld,
+                            int box_rows, int dtype) {
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)plane_ld * 2};
+  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, 1u};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&map,
+                           dtype == EET_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                           3, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  EET_REQUIRE(r == CUDA_SUCCESS, EET_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed");
+  return map;
+}
+
 int device_sm_count() {
   static int n = 0;
   if (n == 0) {

@@ -366,6 +366,18 @@ int eet_pool_stats(eet_pool* pool, uint64_t stats[4]) {
   EET_API_END
 }
 
+int eet_pool_debug_fill(eet_pool* pool, int value) {
+  EET_API_BEGIN
+  EET_CHECK_CUDA(cudaDeviceSynchronize());
+  for (auto& b : pool->bufs) {
+    if (!b.idle) continue;
+    if (pool->device) EET_CHECK_CUDA(cudaMemset(b.ptr, value & 0xFF, b.cap));
+    else std::memset(b.ptr, value & 0xFF, b.cap);
+  }
+  EET_CHECK_CUDA(cudaDeviceSynchronize());
+  EET_API_END
+}
+
 int eet_pool_ledger_size(eet_pool* pool, size_t* n) {
   EET_API_BEGIN
   *n = pool->ledger.size();

@@ -11,6 +11,10 @@ namespace eet {
 // host: 2-D K-major TMA map (rows x K, pitch ld elements, box 64 x box_rows,
 // 128B swizzle, OOB zero fill) and the SM count of the current device
 CUtensorMap make_tma_map_2d(const void* ptr, int rows, int K, int ld, int box_rows, int dtype);
+// 3-D map [planes][rows][K], plane pitch plane_ld elements, rows past `rows`
+// zero-filled (bounded K/V windows of the cache)
+CUtensorMap make_tma_map_3d(const void* ptr, int planes, int rows, int K, long long plane_ld,
+                            int box_rows, int dtype);
 int device_sm_count();
 
 namespace sm100 {
@@ -74,6 +78,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {

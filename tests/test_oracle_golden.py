@@ -110,3 +110,39 @@ def test_plumbing_vectors():
     assert orc.left_pads([5, 2, 4, 10]) == tuple(g["make_batch_5_2_4_10"])
     assert orc.lengths_for_ratio(4, 64, 0.2) == list(g["ratio_lengths_4_64_02"])
     assert orc.lengths_for_ratio(8, 512, 0.5) == list(g["ratio_lengths_8_512_05"])
+
+
+def test_teacher_forcing_with_own_tokens_is_identity():
+    """Forcing the reference's own tokens reproduces the free-running
+    generate exactly (the forced mode only changes what is fed back)."""
+    g = load_golden("generate")
+    key, m = next(iter(golden_meta(g).items()))
+    model = orc.seeded_weights(m["hidden"], m["layers"], m["heads"], m["vocab"], m["max_sequence"], m["seed"])
+    prompts = [[int(t) for t in row if t >= 0] for row in g[f"{key}_prompts"]]
+    toks, logs = orc.generate(model, prompts, m["steps"], m["max_sequence"], collect_logits=True)
+    ft, flogs = orc.generate(model, prompts, m["steps"], m["max_sequence"], collect_logits=True, forced=toks)
+    assert np.array_equal(ft, toks)
+    assert all(np.array_equal(a, b) for a, b in zip(logs, flogs))
+    # forcing other tokens changes later logits but step 0 stays put
+    other = (toks + 1) % m["vocab"]
+    _, olog = orc.generate(model, prompts, m["steps"], m["max_sequence"], collect_logits=True, forced=other)
+    assert np.array_equal(olog[0], logs[0])
+
+
+def test_layer_rows_equals_full_layer():
+    """decoder_layer_rows (selected query slots) is bit-identical to the full
+    prompt-phase layer on those slots, and writes the same K/V."""
+    h, heads, s = 64, 4, 40
+    model = orc.seeded_weights(h, 1, heads, 8, s + 1, 5)
+    x = np.random.default_rng(1).normal(size=(3, s, h)).astype(np.float32)
+    pads = (0, 9, 39)
+    kv = orc.OracleKV(3, heads, s + 1, h // heads, 1)
+    full = orc.decoder_layer(x, model.layers[0], kv, pads, 0, heads)
+    rows = [0, 8, 9, 21, 39]
+    kv2 = orc.OracleKV(3, heads, s + 1, h // heads, 1)
+    part = orc.decoder_layer_rows(x, model.layers[0], pads, heads, rows, kv=kv2)
+    for b, pad in enumerate(pads):
+        for j, r in enumerate(rows):
+            if r >= pad:
+                assert np.array_equal(part[b, j], full[b, r])
+    assert np.array_equal(kv.k[0], kv2.k[0]) and np.array_equal(kv.v[0], kv2.v[0])
