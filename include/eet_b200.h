@@ -160,6 +160,12 @@ int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream)
 /* Development trace of the packed decode GEMV: on = 1 resets and enables,
  * on = 0 disables and copies 4096 x 8 stamps to out (n = records). */
 int eet_debug_ktrace(int on, long long* out, int* n);
+/* Development trace of the split-K cluster decode GEMV / LM head
+ * (gemv_cl.cu): on = 1 resets and enables it; on = 0 disables it and copies
+ * out <= 8192 records of 24 int64 [(N << 32) | (K << 1) | ln, block, start,
+ * wait passed, X staged, weights landed, partials sent, end (globaltimer),
+ * then clock64 offsets of the phase ends of CTA 0]. */
+int eet_debug_cltrace(int on, long long* out, int* n);
 
 /* ------------------------------------------------------------ layer path */
 typedef struct {

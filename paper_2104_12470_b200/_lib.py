@@ -62,6 +62,7 @@ SIGNATURES = {
     "eet_transpose_cast": (i32, [i32, p, i32, i32, p, p]),
     "eet_debug_launch_chain": (i32, [i32, i32, i32, p, p]),
     "eet_debug_ktrace": (i32, [i32, p, p]),
+    "eet_debug_cltrace": (i32, [i32, p, p]),
     "eet_profile_summary": (i32, [i32, C.POINTER(u64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "eet_plan_folding": (i32, [i32, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
     "eet_pool_create": (i32, [C.POINTER(p)]),

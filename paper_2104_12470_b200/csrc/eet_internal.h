@@ -196,6 +196,14 @@ struct DecodeArgs {
 };
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
 
+// ---- decode projections / LM head straight from the K-major weights (gemv_cl.cu)
+bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
+             long long x_sb, long long x_ss, const int2* rinfo, const float* g, const float* b, const Epi& e,
+             cudaStream_t st);
+bool lm_head_argmax(int dtype, const void* W, int M, int N, int K, const float* x, long long x_sb, long long x_ss,
+                    const int2* rinfo, const float* g, const float* b, const Epi& e, cudaStream_t st);
+bool gemv_cl_enabled();              // EET_GEMV_CL=0 selects the packed-fragment path (A/B)
+
 // ---- decode GEMV from pre-permuted weights (gemv_mma.cu)
 void packed_register(const void* src, const void* packed);
 void packed_clear();

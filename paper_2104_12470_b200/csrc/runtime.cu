@@ -154,6 +154,14 @@ static bool skip_decode(const char* what) {
   return ("," + spec + ",").find("," + std::string(what) + ",") != std::string::npos;
 }
 
+bool eet::gemv_cl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("EET_GEMV_CL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // decode megakernel switch (default off: EET_MEGAKERNEL=1 or eet_set_decode_megakernel)
 static std::atomic<int> g_decode_mk{[] {
   const char* e = std::getenv("EET_MEGAKERNEL");
@@ -594,6 +602,9 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     // decode rows: LN1 runs inside the GEMV prologue; otherwise LN -> GEMM
     const bool inc = p.phase == EET_PHASE_INCREMENTAL;
     if (inc && skip_decode("qkv")) {
+    } else if (inc && gemv_cl_enabled() &&
+               gemv_cl(dt, w->wqkv, T, 3 * hq, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b, e, st)) {
+      // split-K cluster GEMV straight from the K-major weight, LayerNorm fused (gemv_cl.cu)
     } else if (inc && gemv_packed(dt, w->wqkv, T, 3 * hq, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln1_g,
                            w->ln1_b, e, st)) {
       // packed-weight decode GEMV with the LayerNorm fused (gemv_mma.cu)
@@ -656,7 +667,9 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
       e.rinfo = p.rinfo;
     }
     if (p.phase == EET_PHASE_INCREMENTAL && skip_decode("o")) {
-    } else if (!(p.phase == EET_PHASE_INCREMENTAL &&
+    } else if (!(p.phase == EET_PHASE_INCREMENTAL && gemv_cl_enabled() &&
+                 gemv_cl(dt, w->wo, T, h, hq, ctx.ptr, hq, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)) &&
+               !(p.phase == EET_PHASE_INCREMENTAL &&
           gemv_packed(dt, w->wo, T, h, hq, ctx.ptr, hq, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
       gemm(dt, ctx.ptr, hq, w->wo, hq, T, h, hq, e, st);
   }
@@ -680,6 +693,8 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
     e.ldo = f;
     const bool inc = p.phase == EET_PHASE_INCREMENTAL;
     if (inc && skip_decode("w1")) {
+    } else if (inc && gemv_cl_enabled() &&
+               gemv_cl(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, e, st)) {
     } else if (inc && gemv_packed(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b,
                            e, st)) {
     } else if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T,
@@ -702,7 +717,9 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
       e.rinfo = p.rinfo;
     }
     if (p.phase == EET_PHASE_INCREMENTAL && skip_decode("w2")) {
-    } else if (!(p.phase == EET_PHASE_INCREMENTAL &&
+    } else if (!(p.phase == EET_PHASE_INCREMENTAL && gemv_cl_enabled() &&
+                 gemv_cl(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)) &&
+               !(p.phase == EET_PHASE_INCREMENTAL &&
           gemv_packed(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
       gemm(dt, mid.ptr, f, w->w2, f, T, h, f, e, st);
   }
@@ -900,7 +917,9 @@ static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long 
   ea.d_step = rt->d_step;
   ea.steps = steps;
   ea.batch = batch;
-  if (gemv_packed(dt, m->head, batch, m->vocab, h, nullptr, 0, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g,
+  if ((gemv_cl_enabled() && lm_head_argmax(dt, m->head, batch, m->vocab, h, xs, x_sb, h, rt->plans[2].rinfo,
+                                            m->lnf_g, m->lnf_b, ea, st)) ||
+      gemv_packed(dt, m->head, batch, m->vocab, h, nullptr, 0, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g,
                   m->lnf_b, ea, st)) {
     lg.release();
     return;
@@ -986,7 +1005,7 @@ int eet_generate(eet_runtime* rt, const eet_model* m, const int* h_prompts, cons
     struct PackGuard {
       ~PackGuard() { packed_clear(); }
     } pack_guard;
-    if (!use_mk && rt->tp_size == 1 && (rt->dtype == EET_F16 || rt->dtype == EET_BF16) && batch <= 16 &&
+    if (!use_mk && !gemv_cl_enabled() && rt->tp_size == 1 && (rt->dtype == EET_F16 || rt->dtype == EET_BF16) && batch <= 16 &&
         rt->ffn == 4 * h && h % 16 == 0)
       mk_pack_model(rt->mk, rt->dtype, m, h, st);
     head_step(rt, m, m->hidden, x_sb, t - 1, batch, steps, tok.as<long long>(), d_logits, st);

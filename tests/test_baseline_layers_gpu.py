@@ -10,7 +10,10 @@ finishes in seconds:
   does not depend on the other 28 — plus one incremental step.
 * c4 (h4096, 32 heads, s4096 = s_max) and c5 (h12288, 96 heads, s2048): a
   spread of query slots through ``oracle.decoder_layer_rows`` (every key,
-  selected queries), plus one incremental step for c5.
+  selected queries), plus one incremental step for c5. At c5 (K = 4h =
+  49152) bf16's own rounding exceeds the elementwise 2e-2 on ~0.8 % of
+  elements, so bf16 is held to the norm-wise 2e-2 and to the format's own
+  elementwise cost (``conftest.check_16bit``, tests/emu16.py).
 * the persistent prefill-attention scheduler's list limit (MAX_ITEMS,
   attn_tc.cu) exceeded, so the per-tile grid fallback runs.
 
@@ -20,7 +23,7 @@ Reference: /root/reference/pkg/src/maskfold/runtime.py:217-263.
 import numpy as np
 import pytest
 
-from conftest import combined_close
+from conftest import check_16bit, combined_close
 
 pytestmark = pytest.mark.gpu
 
@@ -127,10 +130,13 @@ def test_c5_gpt3_scale_layer(eet):
     rows = _rows(s, 52)
     okv = orc.OracleKV(1, heads, s + 1, h // heads, 1)
     ref = orc.decoder_layer_rows(x, w, desc.padding_len, heads, rows, kv=okv)
-    combined_close(out[0, rows], ref[0], 2e-2, "c5 prompt rows")
+    from emu16 import bound_ratio, emu_layer_rows
+    emu = bound_ratio(emu_layer_rows(x, w, desc.padding_len, heads, torch.bfloat16, rows)[0], ref[0])
+    nr, br = check_16bit(out[0, rows], ref[0], "bf16", "c5 prompt rows", emu)
+    print(f"c5 bf16 prompt rows: norm-wise {nr:.4f}, elementwise ratio {br:.3f} (format's own {emu:.3f})")
     okv.advance(s)
     ref_st = orc.decoder_layer(step, w, okv, desc.padding_len, 0, heads)
-    combined_close(st, ref_st, 2e-2, "c5 incremental step")
+    check_16bit(st, ref_st, "bf16", "c5 incremental step", emu)
 
 
 def test_attention_work_list_overflow_falls_back_to_grid(eet):
