@@ -74,13 +74,13 @@ def peaks():
 
 
 def lengths_for(w):
-    from oracle import eet_oracle as orc
+    from paper_2104_12470_b200.report import prompt_lengths_for_ratio
     b, s = w["batch"], w["prompt"]
     spec = w.get("lengths", "full")
     if spec == "full":
         return [s] * b
     if spec == "ratio0.2":
-        return orc.lengths_for_ratio(b, s, 0.2)
+        return prompt_lengths_for_ratio(b, s, 0.2)
     if spec == "ragged3":
         return [s] + [int(v) for v in np.random.default_rng(3).integers(1, s + 1, b - 1)]
     raise ValueError(spec)
@@ -202,6 +202,109 @@ def cpu_generate_sample(w, reps: int = 1):
     return b * steps / best, sample
 
 
+def reference_module():
+    """The unmodified reference (``maskfold``) installed under baseline/_ref
+    (pip --target), or None when it is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "maskfold")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import maskfold
+        return maskfold
+    except Exception:
+        return None
+
+
+def ref_generate_sample(mf, w):
+    """Bounded sample of the REAL reference generate path (maskfold from
+    baseline/_ref: numpy + OpenBLAS on all host cores), through its own
+    decoder_layer_forward / head_logits (runtime.py:217-263, :341-344):
+    one prompt layer + 2 decode layer steps at the mean cache length + 2
+    heads, extrapolated to L layers x steps like cpu_generate_sample."""
+    b, h, heads, V, p, steps, L = (w["batch"], w["hidden"], w["heads"], w["vocab"], w["prompt"],
+                                   w["steps"], w["layers"])
+    cfg = mf.ModelConfig(batch_size=b, hidden_size=h, layer_count=1, head_count=heads, max_prompt=p,
+                         max_sequence=w["max_seq"])
+    model = mf.random_weights(cfg, V, 0)
+    kv, acts = mf.preallocate_caches(cfg)
+    pool = mf.BufferPool()
+    desc = mf.make_batch([p] * b)
+    x = np.random.default_rng(0).normal(0, 1, size=(b, p, h)).astype(np.float32)
+    t0 = time.perf_counter()
+    mf.decoder_layer_forward(x, model.layers[0], kv, desc, mf.Phase.PROMPT_PARALLEL, pool, acts, 0)
+    t_prompt = time.perf_counter() - t0
+    Lmean = p + steps // 2
+    kv.advance(Lmean - 1 - kv.filled)
+    x1 = np.ascontiguousarray(x[:, :1])
+    t0 = time.perf_counter()
+    for _ in range(2):
+        mf.decoder_layer_forward(x1.copy(), model.layers[0], kv, desc, mf.Phase.INCREMENTAL, pool, acts, 0)
+    t_step = (time.perf_counter() - t0) / 2
+    t0 = time.perf_counter()
+    for _ in range(2):
+        np.argmax(mf.runtime.head_logits(model, x[:, -1]), axis=1)
+    t_head = (time.perf_counter() - t0) / 2
+    total = L * t_prompt + t_head + steps * (L * t_step + t_head)
+    sample = (f"reference maskfold (baseline/_ref): 1 prompt layer (b{b} s{p}) + 2 decode layer steps at "
+              f"cache length {Lmean} + 2 LM heads, extrapolated x{L} layers x{steps} steps")
+    return b * steps / total, sample
+
+
+def ref_layer_sample(mf, w):
+    """One PROMPT_PARALLEL layer of the REAL reference (maskfold), bounded
+    like cpu_layer_sample (one sequence, scaled, when the batch is large)."""
+    lens = lengths_for(w)
+    b, h, heads = w["batch"], w["hidden"], w["heads"]
+    if b * max(lens) * h > 16 * 1024 * 1024 or h >= 4096:
+        lens1, scaled = [max(lens)], True
+        if h >= 4096:                                  # keep the sample in the 10-30 s range
+            lens1 = [min(max(lens), 1024 if h <= 4096 else 512)]
+    else:
+        lens1, scaled = lens, False
+    s = max(lens1)
+    cfg = mf.ModelConfig(batch_size=len(lens1), hidden_size=h, layer_count=1, head_count=heads, max_prompt=s,
+                         max_sequence=s)
+    # N(0, 0.02^2) float32 draws (the reference's float64 init takes ~1 min at
+    # h12288; values do not change the time), reference field order
+    rng = np.random.default_rng(0)
+    mat = lambda *sh: rng.standard_normal(size=sh, dtype=np.float32) * np.float32(0.02)  # noqa: E731
+    one, zero = np.ones(h, np.float32), np.zeros(h, np.float32)
+    lw = mf.LayerWeights(one, zero, mat(h, h), mat(h, h), mat(h, h), mat(h, h), one.copy(), zero.copy(),
+                         mat(h, 4 * h), mat(4 * h, h))
+    kv, acts = mf.preallocate_caches(cfg)
+    desc = mf.make_batch(lens1)
+    x = np.random.default_rng(1).normal(0, 1, size=(len(lens1), s, h)).astype(np.float32)
+    dt = None
+    for _ in range(3 if sum(lens1) * h < 4 * 1024 * 1024 else 1):   # small samples: best of 3
+        t0 = time.perf_counter()
+        mf.decoder_layer_forward(x.copy(), lw, kv, desc, mf.Phase.PROMPT_PARALLEL, mf.BufferPool(), acts, 0)
+        d = time.perf_counter() - t0
+        dt = d if dt is None else min(dt, d)
+    sample = f"reference maskfold (baseline/_ref): one layer over {len(lens1)} sequence(s) of {s}" + (
+        f", scaled to the {b} x {max(lens)} workload by valid-token rate" if scaled else "")
+    return sum(lens1) / dt, sample
+
+
+def cpu_baseline_sample(w):
+    """(tokens/s, sample, kind): the real reference when installed, else the
+    oracle port of it."""
+    mf = reference_module()
+    kind = w.get("kind", "generate")
+    if mf is not None:
+        # warm numpy / OpenBLAS threads outside the sample (first call ~1 s)
+        wcfg = mf.ModelConfig(batch_size=1, hidden_size=64, layer_count=1, head_count=4, max_prompt=16,
+                              max_sequence=16)
+        wkv, wacts = mf.preallocate_caches(wcfg)
+        mf.decoder_layer_forward(np.ones((1, 16, 64), np.float32), mf.random_weights(wcfg, 8, 0).layers[0], wkv,
+                                 mf.make_batch([16]), mf.Phase.PROMPT_PARALLEL, mf.BufferPool(), wacts, 0)
+        v, sample = ref_generate_sample(mf, w) if kind == "generate" else ref_layer_sample(mf, w)
+        return v, sample, "reference"
+    v, sample = cpu_generate_sample(w) if kind == "generate" else cpu_layer_sample(w)
+    return v, sample, "port"
+
+
 def cpu_layer_sample(w):
     """One PROMPT_PARALLEL decoder layer on the oracle port: valid tokens/s."""
     from oracle import eet_oracle as orc
@@ -226,6 +329,57 @@ def cpu_layer_sample(w):
     return sum(lens1) / dt, sample          # time is linear in tokens: same rate
 
 
+def measure_fp32_peak(torch):
+    torch.backends.cuda.matmul.allow_tf32 = False
+    a = torch.randn(8192, 8192, device="cuda")
+    b = torch.randn(8192, 8192, device="cuda")
+    best = 0.0
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 2 * 8192 ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    del a, b
+    return best
+
+
+def ablation_roofline(step, args, ms_full, w, hbm, torch, _lib):
+    """In-graph cost of the decode kernels with programmatic dependent launch
+    intact: the generate time with a kernel class left out of every decode
+    step (eet_debug_skip) subtracted from the full time. Returns
+    {class: (delta ms per generate, algorithmic bytes per generate, launches)}."""
+    h, L, V, es, b = w["hidden"], w["layers"], w["vocab"], 2, w["batch"]
+    steps, p = w["steps"], w["prompt"]
+    classes = {
+        # decode projections (gemv_cl): every weight of every layer once per step
+        "gemv_cl": ("qkv,o,w1,w2", steps * L * 12 * h * h * es, steps * L * 4),
+        # decode attention: every cached K/V row of the batch once per step
+        "attn_decode": ("attn", sum(b * 2 * h * es * L * (p + s + 1) for s in range(steps)), steps * L),
+        # LM head + fused argmax
+        "lm_head": ("head", steps * V * h * es, steps),
+    }
+    out = {}
+    reps = max(2, min(args.steps, 3))
+    for name, (spec, byts, launches) in classes.items():
+        _lib.call("eet_debug_skip", spec.encode())
+        try:
+            step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                step()
+            e1.record()
+            torch.cuda.synchronize()
+        finally:
+            _lib.call("eet_debug_skip", b"")
+        delta = ms_full - e0.elapsed_time(e1) / reps
+        out[name] = (delta, byts, launches)
+    return out
+
+
 # ------------------------------------------------------------------ main
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -238,10 +392,9 @@ def run_reference(args, w, ws, rank):
     if rank != 0:
         return
     reps = []
-    sample = ""
-    kind = w.get("kind", "generate")
+    sample, ckind = "", "port"
     for i in range(args.warmup + args.steps):
-        v, sample = cpu_generate_sample(w) if kind == "generate" else cpu_layer_sample(w)
+        v, sample, ckind = cpu_baseline_sample(w)
         if i >= args.warmup:
             reps.append(v)
     value = statistics.median(reps)
@@ -251,8 +404,9 @@ def run_reference(args, w, ws, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": unit, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded random weights and tokens)",
-        "config": {"workload": w["desc"], "batch": w["batch"]},
-        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
+        "config": {"workload": w["desc"], "batch_per_gpu": w["batch"],
+                   "reference_compute": "float32 numpy (the reference has no 16-bit mode, core.py:20)"},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": ckind,
                          "sample": sample},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -293,9 +447,10 @@ def main():
     hbm, tflops, peak_src = peaks()
     if w["dtype"] == "fp32":
         # fp32 mode runs true-FP32 FFMA on the CUDA cores (no TF32, SURVEY
-        # App. B.4): its roofline is the FP32 SIMT peak, 148 SMs x 128 FMA/clk
-        # x 2 x 1.965 GHz (nominal; not in MEASURED_PEAKS.json)
-        tflops, peak_src = 2 * 148 * 128 * 1.965e9 / 1e12, "nominal FP32 SIMT (148 SM x 128 FMA/clk x 1.965 GHz)"
+        # App. B.4): its roofline is the FP32 SIMT peak, not in
+        # MEASURED_PEAKS.json, so measured here: cuBLAS fp32 GEMM with TF32
+        # off (SURVEY §8(d) protocol), best of 5 at 8192^3
+        tflops, peak_src = measure_fp32_peak(torch), "measured: torch.matmul fp32, allow_tf32=False, 8192^3"
     if kind == "generate":
         cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=w["layers"],
                               head_count=w["heads"], max_prompt=w["prompt"], max_sequence=w["max_seq"],
@@ -420,8 +575,11 @@ def main():
         torch.cuda.synchronize()
         extra["latency_b1_s"] = time.perf_counter() - t0
 
-    roofline, kernels = None, {}
+    roofline, kernels, ablation = None, {}, {}
     if not args.no_profile and rank == 0:
+        # per-kernel view from a profiled replay: CUDA events around every
+        # launch (in the decode graph they sit between PDL-linked kernels and
+        # break the overlap, so these are per-launch upper bounds)
         _lib.profile_enable(True)
         step(graph=True)
         torch.cuda.synchronize()
@@ -434,21 +592,38 @@ def main():
             kernels[name] = {"launches": n, "ms": round(kms, 4), "share": round(kms / total, 4),
                              "achieved": round(ach, 2), "unit": "GB/s" if hbm_k else "TFLOP/s",
                              "frac": round(ach / (hbm if hbm_k else tflops), 4)}
-        dom = max(summ, key=lambda k: summ[k][1])
-        n, kms, by, fl = summ[dom]
-        hbm_k = dom in HBM_KINDS
-        traffic = None
         tf = os.path.join(ROOT, "profiles", "traffic_per_launch.json")
-        if os.path.exists(tf):
-            traffic = json.load(open(tf)).get(args.workload, {}).get(dom)
-        ach = kernels[dom]["achieved"]
-        roofline = {"kernel": dom, "bound": "hbm" if hbm_k else "tensor", "achieved": ach,
-                    "peak": hbm if hbm_k else tflops, "unit": "GB/s" if hbm_k else "TFLOP/s",
-                    "frac": round(ach / (hbm if hbm_k else tflops), 4), "traffic": traffic,
-                    "algorithmic_per_launch": (by if hbm_k else fl) / n,
-                    "avg_launch_us": kms / n * 1e3, "peak_source": peak_src,
-                    "timing": "profiled replay of one step: CUDA events around every launch on its "
-                              "stream (event-record nodes inside the decode graph)"}
+        traffic_tab = json.load(open(tf)).get(args.workload, {}) if os.path.exists(tf) else {}
+        if kind == "generate":
+            # headline roofline from in-graph ablation deltas (PDL intact)
+            ms_gen = ms / args.steps
+            abl = ablation_roofline(step, args, ms_gen, w, hbm, torch, _lib)
+            for name, (dms, byts, nl) in abl.items():
+                ach = byts / (dms / 1e3) / 1e9 if dms > 0 else None
+                ablation[name] = {"ms_per_generate": round(dms, 3), "share": round(dms / ms_gen, 4),
+                                  "launches": nl, "avg_launch_us": round(dms / nl * 1e3, 3),
+                                  "algorithmic_bytes": byts, "achieved": round(ach, 1) if ach else None,
+                                  "unit": "GB/s", "frac": round(ach / hbm, 4) if ach else None}
+            dom = max(ablation, key=lambda k: ablation[k]["ms_per_generate"])
+            a = ablation[dom]
+            roofline = {"kernel": dom, "bound": "hbm", "achieved": a["achieved"], "peak": hbm, "unit": "GB/s",
+                        "frac": a["frac"], "traffic": traffic_tab.get(dom),
+                        "algorithmic_per_launch": a["algorithmic_bytes"] / a["launches"],
+                        "avg_launch_us": a["avg_launch_us"], "peak_source": peak_src,
+                        "timing": "in-graph ablation: device time of the whole generate minus the same with "
+                                  "this kernel class left out of every decode step (eet_debug_skip), CUDA events, "
+                                  "PDL intact; avg_launch_us = that delta / launches"}
+        else:
+            dom = max(summ, key=lambda k: summ[k][1])
+            n, kms, by, fl = summ[dom]
+            hbm_k = dom in HBM_KINDS
+            ach = kernels[dom]["achieved"]
+            roofline = {"kernel": dom, "bound": "hbm" if hbm_k else "tensor", "achieved": ach,
+                        "peak": hbm if hbm_k else tflops, "unit": "GB/s" if hbm_k else "TFLOP/s",
+                        "frac": round(ach / (hbm if hbm_k else tflops), 4), "traffic": traffic_tab.get(dom),
+                        "algorithmic_per_launch": (by if hbm_k else fl) / n,
+                        "avg_launch_us": kms / n * 1e3, "peak_source": peak_src,
+                        "timing": "profiled replay of one layer: CUDA events around every launch on its stream"}
 
     # whole-generate HBM roofline (c2): every decode step must stream all
     # weights once (+ LM head) and every cached K/V row of the batch once
@@ -466,8 +641,8 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        v, sample = cpu_generate_sample(w) if kind == "generate" else cpu_layer_sample(w)
-        cpu = {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port", "sample": sample}
+        v, sample, ckind = cpu_baseline_sample(w)
+        cpu = {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": ckind, "sample": sample}
 
     if rank == 0:
         clocks = clk.summary(clk_lo, clk_hi)
@@ -488,6 +663,8 @@ def main():
             "cpu_baseline": cpu,
             "kernels": kernels,
         }
+        if ablation:
+            line["kernels_in_graph"] = ablation
         if step_roofline:
             line["generate_roofline"] = step_roofline
         line.update(extra)

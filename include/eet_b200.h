@@ -53,11 +53,6 @@ typedef enum { EET_PHASE_PROMPT = 0, EET_PHASE_INCREMENTAL = 1 } eet_phase;
 const char* eet_last_error(void);
 int eet_abi_version(void);
 
-/* Selects the decode path of eet_generate for eligible shapes (16-bit, head
- * dim 64, h <= 2048, batch <= 16): 1 = persistent decode megakernel (one
- * launch per step), 0 = per-op kernels in a CUDA graph (default). Returns
- * the previous setting. New; the reference has a single CPU path. */
-int eet_set_decode_megakernel(int on);
 /* Number of kernel launches issued by this library since load (the bench's
  * gpu_launches evidence). */
 uint64_t eet_launch_count(void);
@@ -146,20 +141,27 @@ int eet_gemm(int dtype, const void* A, const void* B, const float* bias,
  * K-major [out, in] compute layout without a host-side transpose. */
 int eet_transpose_cast(int dtype, const float* src, int rows, int cols, void* dst, void* stream);
 
-/* Decode GEMV through the packed-fragment path (gemv_mma.cu): packs W
- * [N, K] (K-major, 16-bit) and computes out[M, N] = X[M, K] W^T in fp32,
- * M <= 16. repack = 0 reuses the copy packed by an earlier call for the same
- * w. Test / micro-benchmark entry; generate uses the path internally. */
-int eet_gemv_packed(int dtype, const void* w, int N, int K, const void* X, int M,
-                    float* out, int repack, void* stream);
+/* Decode projection kernel of the incremental phase (gemv_cl.cu; the
+ * per-token halves of runtime.py:131-136, :188, :206-213) as a test /
+ * micro-benchmark entry: W [N, K] K-major 16-bit, M <= 16 token rows.
+ * x == NULL: input X [M, K] 16-bit (ld K); x != NULL: input LayerNorm(x)
+ * of fp32 rows x [M, K] (ld K) with g, b [K] (runtime.py:83-94).
+ * mode 0: out = fp32 [M, N]; mode 2: out = 16-bit GELU(.) [M, N];
+ * mode 3: out (fp32 [M, N]) += result (residual). EET_ERR_UNSUPPORTED for
+ * shapes the kernel does not take (K % 64, M > 16, ...). */
+int eet_gemv_decode(int dtype, const void* w, int N, int K, const void* X, const float* x, const float* g,
+                    const float* b, int M, int mode, void* out, void* stream);
+
+/* In-graph ablation for timing: comma list of decode launches to leave out
+ * of eet_generate's decode steps ("qkv,attn,o,w1,w2,head"; "" = none).
+ * Results are wrong while set; bench.py derives per-kernel in-graph times
+ * from the step-time deltas (programmatic dependent launch intact). */
+int eet_debug_skip(const char* spec);
 
 /* Calibration: n dependent launches of an empty kernel (ctas CTAs), with or
  * without programmatic dependent launch; counter may be NULL. */
 int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream);
 
-/* Development trace of the packed decode GEMV: on = 1 resets and enables,
- * on = 0 disables and copies 4096 x 8 stamps to out (n = records). */
-int eet_debug_ktrace(int on, long long* out, int* n);
 /* Development trace of the split-K cluster decode GEMV / LM head
  * (gemv_cl.cu): on = 1 resets and enables it; on = 0 disables it and copies
  * out <= 8192 records of 24 int64 [(N << 32) | (K << 1) | ln, block, start,

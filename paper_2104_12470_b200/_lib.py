@@ -57,12 +57,11 @@ SIGNATURES = {
     "eet_profile_enable": (i32, [i32]),
     "eet_profile_kinds": (i32, []),
     "eet_profile_kind_name": (C.c_char_p, [i32]),
-    "eet_set_decode_megakernel": (i32, [i32]),
-    "eet_gemv_packed": (i32, [i32, p, i32, i32, p, i32, p, i32, p]),
+    "eet_gemv_decode": (i32, [i32, p, i32, i32, p, p, p, p, i32, i32, p, p]),
     "eet_transpose_cast": (i32, [i32, p, i32, i32, p, p]),
     "eet_debug_launch_chain": (i32, [i32, i32, i32, p, p]),
-    "eet_debug_ktrace": (i32, [i32, p, p]),
     "eet_debug_cltrace": (i32, [i32, p, p]),
+    "eet_debug_skip": (i32, [C.c_char_p]),
     "eet_profile_summary": (i32, [i32, C.POINTER(u64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "eet_plan_folding": (i32, [i32, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
     "eet_pool_create": (i32, [C.POINTER(p)]),
@@ -163,8 +162,3 @@ def profile_summary() -> dict:
     return out
 
 
-def set_decode_megakernel(on: bool) -> bool:
-    """Decode path of generate for eligible shapes: True = persistent
-    megakernel (default), False = per-op kernels in a CUDA graph. Returns the
-    previous setting."""
-    return bool(lib().eet_set_decode_megakernel(1 if on else 0))

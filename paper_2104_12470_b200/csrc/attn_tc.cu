@@ -20,6 +20,9 @@
 // one tile while the softmax warps of the other run.
 #include "sm100.cuh"
 
+#include <mutex>
+#include <unordered_map>
+
 #include <cstdlib>
 #include <algorithm>
 #include <atomic>
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (r > 0) mbar_wait(q_empty, (r - 1) & 1);       // sQ free; fetch the next item late
         const int lin = n_work > 0 ? atomicAdd(a.ctr, 1) : (r == 0 ? 0 : 1);
         if (r >= 2) mbar_wait(&it_empty[r & 1], ((r - 2) >> 1) & 1);
-        item_buf[r & 1] = lin;
+        atomicExch(&item_buf[r & 1], lin);              // (mbarrier-ordered; atomic for racecheck)
         mbar_arrive(&it_full[r & 1]);
         Item w;
         if (!decode(lin, w)) break;
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int g0 = 0, cA = 0, cB = 0;                         // item-start counters
       for (int r = 0;; ++r) {
         mbar_wait(&it_full[r & 1], (r >> 1) & 1);
-        const int lin = *reinterpret_cast<volatile int*>(&item_buf[r & 1]);
+        const int lin = atomicAdd(&item_buf[r & 1], 0);
         mbar_arrive(&it_empty[r & 1]);
         Item w;
         if (!decode(lin, w)) break;
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int cb = 0;                                           // this tile's counter at item start
     for (int r = 0;; ++r) {
     mbar_wait(&it_full[r & 1], (r >> 1) & 1);
-    const int lin = *reinterpret_cast<volatile int*>(&item_buf[r & 1]);
+    const int lin = atomicAdd(&item_buf[r & 1], 0);
     __syncwarp();
     if (lane == 0) mbar_arrive(&it_empty[r & 1]);
     Item w;
@@ -591,11 +594,11 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   }();
   a.poly = poly;
   auto kern = attn_tc_kernel<T, HD>;
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [&] {                     // thread-safe one-time init
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   const int npair = (p.seq + 2 * BQ - 1) / (2 * BQ);
   thread_local FaItems items;         // copied into the launch parameters
   a.nitems = 0;
@@ -653,17 +656,24 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
     }
   }
   if (a.nitems > 0) {
-    // counters re-armed by the kernel itself; rotating slots keep launches
-    // on different streams apart
-    constexpr int NSLOT = 64;
-    static int* const ctrs = [] {                     // thread-safe one-time init
-      int* c = nullptr;
-      EET_CHECK_CUDA(cudaMalloc(&c, NSLOT * 2 * sizeof(int)));
-      EET_CHECK_CUDA(cudaMemset(c, 0, NSLOT * 2 * sizeof(int)));
-      return c;
-    }();
-    static std::atomic<unsigned> slot{0};
-    a.ctr = ctrs + 2 * (slot.fetch_add(1, std::memory_order_relaxed) % NSLOT);
+    // work counter: one pair per stream, zeroed on the launch stream before
+    // every launch (stream order keeps launches on one stream apart; other
+    // streams use their own pair)
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, int*> per_stream;
+    int* c = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = per_stream.find(st);
+      if (it == per_stream.end()) {
+        EET_CHECK_CUDA(cudaMalloc(&c, 2 * sizeof(int)));
+        per_stream[st] = c;
+      } else {
+        c = it->second;
+      }
+    }
+    EET_CHECK_CUDA(cudaMemsetAsync(c, 0, 2 * sizeof(int), st));
+    a.ctr = c;
   }
   // list: persistent, one CTA per SM (the smem footprint allows one)
   dim3 grid = a.nitems > 0 ? dim3((unsigned)std::min(a.nitems, device_sm_count()), 1, 1)

@@ -89,7 +89,7 @@ enum EpiMode : int {
   EPI_GELU_T = 2,     // out_T[m*ldo + n]   = gelu(acc + bias)
   EPI_RESID = 3,      // x[b*x_sb + t*x_ss + n] += acc + bias      (row map)
   EPI_QKV = 4,        // n<hq: q_T[m*hq+n]; else K/V cache scatter (row map)
-  EPI_ARGMAX = 5,     // LM head: greedy token per row (gemv_packed only), optional logits
+  EPI_ARGMAX = 5,     // LM head: greedy token per row (lm_head_argmax only), optional logits
 };
 
 struct Epi {
@@ -202,28 +202,7 @@ bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int l
              cudaStream_t st);
 bool lm_head_argmax(int dtype, const void* W, int M, int N, int K, const float* x, long long x_sb, long long x_ss,
                     const int2* rinfo, const float* g, const float* b, const Epi& e, cudaStream_t st);
-bool gemv_cl_enabled();              // EET_GEMV_CL=0 selects the packed-fragment path (A/B)
-
-// ---- decode GEMV from pre-permuted weights (gemv_mma.cu)
-void packed_register(const void* src, const void* packed);
-void packed_clear();
-bool gemv_packed(int dtype, const void* wsrc, int M, int N, int K, const void* X, int ldx,
-                 const float* x, long long x_sb, long long x_ss, const int2* rinfo, const float* g,
-                 const float* b, const Epi& e, cudaStream_t st);
-
-// ---- persistent decode megakernel (decode_mk.cu)
-struct MkState;
-void mk_state_free(MkState* s);
-bool mk_eligible(int dtype, int h, int heads, int batch, int ffn);
-size_t mk_packed_bytes(int N, int K);
-void mk_pack(const void* w, int N, int K, void* out, cudaStream_t st);
-// pack every projection of the model (and the LM head) into st's buffer and
-// register the copies for gemv_packed
-void mk_pack_model(MkState*& st, int dtype, const eet_model* m, int h, cudaStream_t stream);
-void mk_generate(MkState*& st, int dtype, int h, int heads, int bmax, int smax,
-                 const eet_model* m, int batch, const int* d_pads, const int* h_pads, int t,
-                 int* d_filled, int* d_step, int* d_cur, long long* d_tokens, int steps,
-                 float* d_logits, cudaStream_t stream);
+// decode attention split plan (attention.cu)
 int decode_splits(int batch, int heads, int smax, int hd, int es);
 
 // cudaLaunchKernelEx with optional programmatic-dependent-launch edge and
@@ -231,8 +210,8 @@ int decode_splits(int batch, int heads, int smax, int hd, int es);
 // griddepcontrol.wait before touching memory written by earlier kernels.
 bool pdl_enabled();                    // EET_NO_PDL=1 turns the PDL edges off (A/B, debugging)
 template <typename... KArgs, typename... Args>
-inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                      bool pdl, dim3 cluster, Args&&... args) {
+inline void launch_cfg(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       bool pdl, dim3 cluster, bool cluster_attr, Args&&... args) {
   pdl = pdl && pdl_enabled();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -246,7 +225,7 @@ inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
     attrs[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
   }
-  if (cluster.x * cluster.y * cluster.z > 1) {
+  if (cluster_attr) {
     attrs[n].id = cudaLaunchAttributeClusterDimension;
     attrs[n].val.clusterDim.x = cluster.x;
     attrs[n].val.clusterDim.y = cluster.y;
@@ -256,6 +235,19 @@ inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sm
   cfg.attrs = attrs;
   cfg.numAttrs = n;
   EET_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+template <typename... KArgs, typename... Args>
+inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      bool pdl, dim3 cluster, Args&&... args) {
+  launch_cfg(kernel, grid, block, smem, st, pdl, cluster, cluster.x * cluster.y * cluster.z > 1,
+             std::forward<Args>(args)...);
+}
+// kernels that use cluster instructions (barrier.cluster, mapa, st.async):
+// launched as a cluster even when it has one CTA
+template <typename... KArgs, typename... Args>
+inline void launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                           bool pdl, dim3 cluster, Args&&... args) {
+  launch_cfg(kernel, grid, block, smem, st, pdl, cluster, true, std::forward<Args>(args)...);
 }
 
 // dtype helpers

@@ -271,11 +271,11 @@ static void launch(const void* A, int lda, const void* B, int ldb, int M, int N,
   CUtensorMap ma = make_tma_map_2d(A, M, K, lda, BM, dtype);
   CUtensorMap mb = make_tma_map_2d(B, N, K, ldb, BN, dtype);
   auto kern = gemm_tc_kernel<T, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static const bool attr_set = [&] {                 // thread-safe one-time init
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_set = true;
-  }
+    return true;
+  }();
+  (void)attr_set;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = std::min(tiles, device_sm_count());
   // A panel of GM M-tiles <= ~40 MB (a third of L2), GM in [4, 32]

@@ -262,8 +262,10 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
     const uint64_t pol = 0x12F0000000000000ull;              // EVICT_FIRST: read once per step
     for (int b = 0; b < Kc / 64; ++b)
       tma_load_2d(smem + L.w + b * R * 128, &mapW, wbar, k0 + b * 64, r0, pol);
-    if (LN) mbar_expect_tx(sbar, (uint32_t)(C * 16 * 8));
-    mbar_expect_tx(rbar, (uint32_t)(n_own * C * KG * 512));
+    if (C > 1) {                                              // DSMEM arrivals (one-CTA clusters stay local)
+      if (LN) mbar_expect_tx(sbar, (uint32_t)(C * 16 * 8));
+      mbar_expect_tx(rbar, (uint32_t)(n_own * C * KG * 512));
+    }
   }
   constexpr int LNV = NV > 0 ? NV : 1;
   const int lrow = threadIdx.x >> 4, lsub = threadIdx.x & 15;  // LN: 16 threads per token row
@@ -329,9 +331,14 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
         if (trace) cy[3] = (q == 1.2345e-30f) ? 0 : cyc();
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // peers' barriers initialised
         if (trace) cy[4] = cyc();
-        if (lsub < C)                                                          // all-gather (mean, M2)
-          st_async_v2(dsmem_addr(smem_u32(stats + rank * 16 + lrow), lsub), mu, q, dsmem_addr(smem_u32(sbar), lsub));
-        mbar_wait(sbar, 0);
+        if (C > 1) {
+          if (lsub < C)                                                        // all-gather (mean, M2)
+            st_async_v2(dsmem_addr(smem_u32(stats + rank * 16 + lrow), lsub), mu, q, dsmem_addr(smem_u32(sbar), lsub));
+          mbar_wait(sbar, 0);
+        } else {                                                               // one-CTA cluster: local
+          if (lsub == 0) stats[lrow] = make_float2(mu, q);
+          __syncthreads();
+        }
         if (trace) cy[5] = cyc();
       }
       // combine the C equal-size slices in rank order: identical in every CTA
@@ -374,9 +381,10 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
         if (r < sh.M && !dry) v = *reinterpret_cast<const uint4*>(X + (size_t)r * sh.ldx + k0 + c * 8);
         *reinterpret_cast<uint4*>(xs + r * xst + c * 8) = v;
       }
-      if (!dry) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
+    __syncwarp();
     __syncthreads();
+    if (!LN && !dry) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // before any DSMEM store
     if (!dry) {
       if (trace) { ts[2] = gtime(); cy[6] = cyc(); }
       mbar_wait(wbar, 0);
@@ -395,13 +403,16 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
       for (int nb = 0; nb < NB; ++nb) {
         const int q = t * NB + nb;
         const int owner = q % C, j = q / C;
-        const float4* dst = recv + ((size_t)(rank * KG + kg) * per_owner + j) * 32 + lane;
-        if (!dry) st_async_v4(dsmem_addr(smem_u32(dst), owner), acc[nb], dsmem_addr(smem_u32(rbar), owner));
+        float4* dst = recv + ((size_t)(rank * KG + kg) * per_owner + j) * 32 + lane;
+        if (dry) continue;
+        if (C > 1) st_async_v4(dsmem_addr(smem_u32(dst), owner), acc[nb], dsmem_addr(smem_u32(rbar), owner));
+        else *dst = make_float4(acc[nb][0], acc[nb][1], acc[nb][2], acc[nb][3]);
       }
     }
     if (!dry) {
       if (trace) { ts[4] = gtime(); cy[9] = cyc(); }
-      if (n_own > 0) mbar_wait(rbar, 0);
+      if (C == 1) __syncthreads();                     // local partials
+      else if (n_own > 0) mbar_wait(rbar, 0);
       if (trace) cy[10] = cyc();
     }
 
@@ -690,7 +701,7 @@ static void launch(const CUtensorMap& mw, const LnSrc& ln, const Shape& sh, size
     while (cur < smem && !set.compare_exchange_weak(cur, smem)) {}
   }
   const int G = (sh.N + 16 * sh.NT - 1) / (16 * sh.NT);
-  launch_ex(kern, dim3(G * sh.C), dim3(THREADS), smem, st, true, dim3(sh.C, 1, 1), mw, ln, sh, e);
+  launch_cluster(kern, dim3(G * sh.C), dim3(THREADS), smem, st, true, dim3(sh.C, 1, 1), mw, ln, sh, e);
   EET_LAUNCH_CHECK();
 }
 
@@ -708,6 +719,8 @@ static void go(const CUtensorMap& mw, const LnSrc& ln, const Shape& sh, size_t s
     const bool small = sh.Kc <= 128;                 // LayerNorm slice: 2 (else 8) float4 per thread
     if (e.mode == EPI_QKV) {
       small ? go_t<T, NB, 2, EPI_QKV>(mw, ln, sh, smem, e, st) : go_t<T, NB, 8, EPI_QKV>(mw, ln, sh, smem, e, st);
+    } else if (e.mode == EPI_STORE_F32) {             // test entry (eet_gemv_decode)
+      small ? go_t<T, NB, 2, EPI_STORE_F32>(mw, ln, sh, smem, e, st) : go_t<T, NB, 8, EPI_STORE_F32>(mw, ln, sh, smem, e, st);
     } else {
       small ? go_t<T, NB, 2, EPI_GELU_T>(mw, ln, sh, smem, e, st) : go_t<T, NB, 8, EPI_GELU_T>(mw, ln, sh, smem, e, st);
     }
@@ -733,7 +746,7 @@ bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int l
              cudaStream_t st) {
   if (dtype != EET_F16 && dtype != EET_BF16) return false;
   const bool ln = x != nullptr;
-  if (ln ? (e.mode != EPI_QKV && e.mode != EPI_GELU_T)
+  if (ln ? (e.mode != EPI_QKV && e.mode != EPI_GELU_T && e.mode != EPI_STORE_F32)
          : (e.mode != EPI_RESID && e.mode != EPI_STORE_F32 && e.mode != EPI_STORE_T && e.mode != EPI_GELU_T))
     return false;
   if (ln && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(b)) & 15 ||
@@ -813,6 +826,29 @@ bool lm_head_argmax(int dtype, const void* W, int M, int N, int K, const float* 
 }  // namespace eet
 
 namespace eet {
+extern "C" int eet_gemv_decode(int dtype, const void* w, int N, int K, const void* X, const float* x, const float* g,
+                               const float* b, int M, int mode, void* out, void* stream) {
+  try {
+    EET_REQUIRE(dtype == EET_F16 || dtype == EET_BF16, EET_ERR_ARG, "gemv_decode: 16-bit dtypes only");
+    EET_REQUIRE(mode == EPI_STORE_F32 || mode == EPI_GELU_T || mode == EPI_RESID, EET_ERR_ARG, "gemv_decode: mode");
+    EET_REQUIRE(!(x && mode == EPI_RESID), EET_ERR_ARG, "gemv_decode: LayerNorm input with residual mode");
+    Epi e;
+    e.mode = mode;
+    if (mode == EPI_RESID) {
+      e.x = reinterpret_cast<float*>(out);
+      e.x_sb = N;
+    } else {
+      e.out = out;
+      e.ldo = N;
+    }
+    const bool ok = gemv_cl(dtype, w, M, N, K, X, K, x, K, 0, nullptr, g, b, e, reinterpret_cast<cudaStream_t>(stream));
+    EET_REQUIRE(ok, EET_ERR_UNSUPPORTED, "gemv_decode: unsupported shape");
+    return EET_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
+}
+
 extern "C" int eet_debug_cltrace(int on, long long* out, int* n) {
   // on = 1: reset + enable; on = 0: disable and copy out (8192 x 8)
   try {

@@ -29,6 +29,7 @@
 #include "sm100.cuh"
 
 #include <map>
+#include <mutex>
 
 namespace eet {
 namespace gv {
@@ -292,6 +293,8 @@ static void plan_splits(int rbs, int nkb, bool lnx, int* splits, int* kbps, F ma
 template <typename Kern>
 static int active_clusters(Kern kern, int smem, int s) {
   static std::map<std::pair<const void*, int>, int> cache;   // (kernel, s)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
   const auto key = std::make_pair(reinterpret_cast<const void*>(kern), s);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
@@ -322,12 +325,12 @@ static void launch(const void* A, int lda, const LnSrc& ln, const void* B, int l
   const int rbs = (N + ROWS - 1) / ROWS;
   const int nkb = (K + BK - 1) / BK;
   auto kern = gemv_tc_kernel<T, MN, LNX>;
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [&] {                     // thread-safe one-time init
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   int splits, kbps;
   plan_splits(rbs, nkb, LNX, &splits, &kbps, [&](int s) { return active_clusters(kern, L::SMEM, s); });
   EET_REQUIRE(splits <= 8, EET_ERR_UNSUPPORTED, "gemv_tc: K too long for one cluster");

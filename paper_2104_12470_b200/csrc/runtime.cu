@@ -10,6 +10,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <mutex>
 #include <vector>
 
 namespace eet {
@@ -143,42 +144,33 @@ using namespace eet;
 
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Development ablation: EET_SKIP=qkv,attn,o,w1,w2,head skips those decode
-// launches (results become wrong; used only to time their in-graph cost).
+// Ablation for in-graph timing (bench.py roofline, tools/decode_step_time.py):
+// EET_SKIP or eet_debug_skip("qkv,attn,o,w1,w2,head") leaves those decode
+// launches out of the step (results become wrong; only their in-graph cost
+// is measured this way, with programmatic dependent launch intact).
+static std::mutex g_skip_mu;
+static std::string g_skip = [] {
+  const char* e = std::getenv("EET_SKIP");
+  return std::string(e ? e : "");
+}();
 static bool skip_decode(const char* what) {
-  static const std::string spec = [] {
-    const char* e = std::getenv("EET_SKIP");
-    return std::string(e ? e : "");
-  }();
-  if (spec.empty()) return false;
-  return ("," + spec + ",").find("," + std::string(what) + ",") != std::string::npos;
+  std::lock_guard<std::mutex> lk(g_skip_mu);
+  if (g_skip.empty()) return false;
+  return ("," + g_skip + ",").find("," + std::string(what) + ",") != std::string::npos;
 }
-
-bool eet::gemv_cl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("EET_GEMV_CL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
-// decode megakernel switch (default off: EET_MEGAKERNEL=1 or eet_set_decode_megakernel)
-static std::atomic<int> g_decode_mk{[] {
-  const char* e = std::getenv("EET_MEGAKERNEL");
-  return (e && e[0] == '1') ? 1 : 0;
-}()};
 
 extern "C" {
 
 const char* eet_last_error(void) { return t_err.c_str(); }
 int eet_abi_version(void) { return 1; }
 
-int eet_set_decode_megakernel(int on) {
-  const int prev = g_decode_mk.load();
-  g_decode_mk.store(on != 0);
-  return prev;
-}
 uint64_t eet_launch_count(void) { return g_launches.load(); }
+
+int eet_debug_skip(const char* spec) {
+  std::lock_guard<std::mutex> lk(g_skip_mu);
+  g_skip = spec ? spec : "";
+  return EET_OK;
+}
 
 int eet_profile_enable(int on) {
   EET_API_BEGIN
@@ -508,7 +500,6 @@ struct eet_runtime {
   int* d_cur = nullptr;               // [bmax]
   int* h_prompts = nullptr;           // pinned staging: prompts in, tokens out
   long long* h_tokens = nullptr;
-  MkState* mk = nullptr;              // decode megakernel state (packed weights, scratch)
   float* xdec = nullptr;              // decode residual stream [bmax, h]
   int2* cand = nullptr;               // fused LM-head argmax candidates
   int* cand_ticket = nullptr;
@@ -521,7 +512,6 @@ struct eet_runtime {
     return p;
   }
   ~eet_runtime() {
-    if (mk) mk_state_free(mk);
     for (void* p : owned) cudaFree(p);
     if (h_prompts) cudaFreeHost(h_prompts);
     if (h_tokens) cudaFreeHost(h_tokens);
@@ -602,12 +592,9 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     // decode rows: LN1 runs inside the GEMV prologue; otherwise LN -> GEMM
     const bool inc = p.phase == EET_PHASE_INCREMENTAL;
     if (inc && skip_decode("qkv")) {
-    } else if (inc && gemv_cl_enabled() &&
-               gemv_cl(dt, w->wqkv, T, 3 * hq, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b, e, st)) {
+    } else if (inc && gemv_cl(dt, w->wqkv, T, 3 * hq, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b,
+                              e, st)) {
       // split-K cluster GEMV straight from the K-major weight, LayerNorm fused (gemv_cl.cu)
-    } else if (inc && gemv_packed(dt, w->wqkv, T, 3 * hq, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln1_g,
-                           w->ln1_b, e, st)) {
-      // packed-weight decode GEMV with the LayerNorm fused (gemv_mma.cu)
     } else if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b, w->wqkv, h,
                                              T, 3 * hq, h, e, st))) {
       Claim ln(rt->pool, (size_t)T * h * es, scope, "attention.layernorm");
@@ -667,10 +654,8 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
       e.rinfo = p.rinfo;
     }
     if (p.phase == EET_PHASE_INCREMENTAL && skip_decode("o")) {
-    } else if (!(p.phase == EET_PHASE_INCREMENTAL && gemv_cl_enabled() &&
-                 gemv_cl(dt, w->wo, T, h, hq, ctx.ptr, hq, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)) &&
-               !(p.phase == EET_PHASE_INCREMENTAL &&
-          gemv_packed(dt, w->wo, T, h, hq, ctx.ptr, hq, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
+    } else if (!(p.phase == EET_PHASE_INCREMENTAL &&
+                 gemv_cl(dt, w->wo, T, h, hq, ctx.ptr, hq, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
       gemm(dt, ctx.ptr, hq, w->wo, hq, T, h, hq, e, st);
   }
   ctx.release();
@@ -693,10 +678,7 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
     e.ldo = f;
     const bool inc = p.phase == EET_PHASE_INCREMENTAL;
     if (inc && skip_decode("w1")) {
-    } else if (inc && gemv_cl_enabled() &&
-               gemv_cl(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, e, st)) {
-    } else if (inc && gemv_packed(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b,
-                           e, st)) {
+    } else if (inc && gemv_cl(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, e, st)) {
     } else if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T,
                                              f, h, e, st))) {
       Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
@@ -717,10 +699,8 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
       e.rinfo = p.rinfo;
     }
     if (p.phase == EET_PHASE_INCREMENTAL && skip_decode("w2")) {
-    } else if (!(p.phase == EET_PHASE_INCREMENTAL && gemv_cl_enabled() &&
-                 gemv_cl(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)) &&
-               !(p.phase == EET_PHASE_INCREMENTAL &&
-          gemv_packed(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
+    } else if (!(p.phase == EET_PHASE_INCREMENTAL &&
+                 gemv_cl(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
       gemm(dt, mid.ptr, f, w->w2, f, T, h, f, e, st);
   }
   mid.release();
@@ -898,6 +878,10 @@ static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long 
   e.ldo = m->vocab;
   // rows (b, slot): the decode plan's row map (b, 0) over x shifted by `slot`
   const float* xs = x + (long long)slot * h;
+  if (x == rt->xdec && skip_decode("head")) {         // ablation: decode-step head
+    lg.release();
+    return;
+  }
   // packed head: argmax fused into the GEMV (no logits round trip)
   const int rtiles = (m->vocab + 15) / 16;
   if (rt->cand_cap < rtiles) {
@@ -917,10 +901,8 @@ static void head_step(eet_runtime* rt, const eet_model* m, const float* x, long 
   ea.d_step = rt->d_step;
   ea.steps = steps;
   ea.batch = batch;
-  if ((gemv_cl_enabled() && lm_head_argmax(dt, m->head, batch, m->vocab, h, xs, x_sb, h, rt->plans[2].rinfo,
-                                            m->lnf_g, m->lnf_b, ea, st)) ||
-      gemv_packed(dt, m->head, batch, m->vocab, h, nullptr, 0, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g,
-                  m->lnf_b, ea, st)) {
+  if (lm_head_argmax(dt, m->head, batch, m->vocab, h, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g, m->lnf_b, ea,
+                     st)) {
     lg.release();
     return;
   } else if (!(batch <= 32 && gemv_tc_ln_sm100(dt, xs, x_sb, h, rt->plans[2].rinfo, m->lnf_g, m->lnf_b,
@@ -999,25 +981,10 @@ int eet_generate(eet_runtime* rt, const eet_model* m, const int* h_prompts, cons
     EET_CHECK_CUDA(cudaMemcpyAsync(rt->d_step, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
     StepPlan& ps = rt->plans[2];
     plan_fill(ps, batch, 1, pads.data(), t, EET_PHASE_INCREMENTAL, st);
-    const bool use_mk = g_decode_mk.load() && rt->tp_size == 1 && mk_eligible(rt->dtype, h, rt->heads, batch, rt->ffn);
-    // decode projections from packed weights (gemv_mma.cu), registered for
-    // this call only
-    struct PackGuard {
-      ~PackGuard() { packed_clear(); }
-    } pack_guard;
-    if (!use_mk && !gemv_cl_enabled() && rt->tp_size == 1 && (rt->dtype == EET_F16 || rt->dtype == EET_BF16) && batch <= 16 &&
-        rt->ffn == 4 * h && h % 16 == 0)
-      mk_pack_model(rt->mk, rt->dtype, m, h, st);
     head_step(rt, m, m->hidden, x_sb, t - 1, batch, steps, tok.as<long long>(), d_logits, st);
-    if (use_mk) {
-      // persistent megakernel: one launch per decode step (decode_mk.cu)
-      mk_generate(rt->mk, rt->dtype, h, rt->heads, rt->bmax, rt->smax, m, batch, ps.pads, pads.data(),
-                  t, rt->d_filled, rt->d_step, rt->d_cur, tok.as<long long>(), steps, d_logits, st);
-    } else {
     // step 0 eagerly (settles every pool buffer), the rest replay one graph
     decode_iteration(rt, m, batch, steps, tok.as<long long>(), d_logits, t + 1, st);
-    }
-    if (steps > 1 && !use_mk) {
+    if (steps > 1) {
       if (use_graph) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;

@@ -235,6 +235,34 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+def _fingerprint(arrays) -> tuple:
+    """Identity + version of the source arrays behind a cached device upload:
+    object id and shape of every array, torch's in-place version counter for
+    tensors, and 8 strided samples of every numpy array (an in-place write
+    that touches none of them goes unseen: call ``invalidate_device_cache``
+    after editing weights in place)."""
+    fp = []
+    for a in arrays:
+        if a is None:
+            fp.append(None)
+            continue
+        if _is_dev(a) or hasattr(a, "_version"):
+            fp.append((id(a), tuple(a.shape), int(a._version)))
+            continue
+        flat = np.asarray(a).reshape(-1)
+        step = max(1, flat.size // 8)
+        fp.append((id(a), flat.shape, flat[::step][:8].tobytes()))
+    return tuple(fp)
+
+
+def invalidate_device_cache(w) -> None:
+    """Drop the device copies cached on a LayerWeights / ModelWeights (and
+    its layers): the next forward / generate uploads the arrays again."""
+    w.__dict__.pop("_eet_device", None)
+    for lw in getattr(w, "layers", []) or []:
+        lw.__dict__.pop("_eet_device", None)
+
+
 class DeviceLayer:
     """One layer's weights in the kernel layout, plus the C struct."""
 
@@ -262,12 +290,16 @@ class DeviceLayer:
 
     @classmethod
     def of(cls, w: LayerWeights, dtype_code: int) -> "DeviceLayer":
-        """Upload once per (weights object, dtype); cached on the object."""
+        """Upload once per (weights object, dtype, source-array fingerprint);
+        cached on the object. The reference reads its arrays on every call
+        (runtime.py:131-212): a replaced or (sampled) modified array uploads
+        again instead of serving stale device weights."""
         cache = w.__dict__.setdefault("_eet_device", {})
-        dl = cache.get(dtype_code)
-        if dl is None:
-            dl = cache[dtype_code] = cls(w, dtype_code)
-        return dl
+        fp = _fingerprint(w.arrays())
+        hit = cache.get(dtype_code)
+        if hit is None or hit[0] != fp:
+            hit = cache[dtype_code] = (fp, cls(w, dtype_code))
+        return hit[1]
 
 
 class DeviceModel:
@@ -291,11 +323,13 @@ class DeviceModel:
 
     @classmethod
     def of(cls, w: ModelWeights, dtype_code: int) -> "DeviceModel":
+        """As DeviceLayer.of: keyed on the fingerprint of every array."""
         cache = w.__dict__.setdefault("_eet_device", {})
-        dm = cache.get(dtype_code)
-        if dm is None:
-            dm = cache[dtype_code] = cls(w, dtype_code)
-        return dm
+        fp = _fingerprint(w.arrays()) + (id(w.layers), len(w.layers))
+        hit = cache.get(dtype_code)
+        if hit is None or hit[0] != fp:
+            hit = cache[dtype_code] = (fp, cls(w, dtype_code))
+        return hit[1]
 
     def cstruct(self, kv, acts, max_prompt: int):
         n = len(self.layers)

@@ -236,3 +236,23 @@ def test_request_validation():
         eet.GenerationRequest(prompts=[[1]], steps=1, strategy="beam")
     with pytest.raises(ValueError):
         eet.GenerationRequest(prompts=[[1]], steps=-1)
+
+
+def test_device_cache_fingerprint_tracks_source_arrays():
+    """the device upload cached on a weights object is keyed
+    on the identity / version of its source arrays, so replacing an array or
+    editing a sampled element re-uploads instead of serving stale weights."""
+    from paper_2104_12470_b200.weights import _fingerprint
+    a = np.arange(1000, dtype=np.float32).reshape(10, 100)
+    b = np.ones(7, dtype=np.float32)
+    fp0 = _fingerprint([a, b])
+    assert _fingerprint([a, b]) == fp0
+    a[0, 0] = -1.0                                   # sampled element (flat index 0)
+    assert _fingerprint([a, b]) != fp0
+    fp1 = _fingerprint([a, b])
+    assert _fingerprint([a.copy(), b]) != fp1        # replaced array
+    import torch
+    t = torch.zeros(4)
+    fpt = _fingerprint([t])
+    t.add_(1.0)                                      # in-place: torch version counter
+    assert _fingerprint([t]) != fpt
