@@ -423,6 +423,9 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--dp", choices=["weak", "strong"], default=None,
+                    help="layer workloads under torchrun: 'strong' shards the workload's batch over the ranks "
+                         "(default for c4), 'weak' gives every rank the whole batch")
     ap.add_argument("--tp", type=int, default=0,
                     help="tensor-parallel layer over the ranks (default: on for c5 under torchrun); "
                          "--tp 1 runs the sharded path on one GPU")
@@ -430,6 +433,8 @@ def main():
     w = dict(WORKLOADS[args.workload])
     if args.batch:
         w["batch"] = args.batch
+    if args.dp is None:
+        args.dp = "strong" if args.workload == "c4" else "weak"
     ws, rank, local = dist_env()
     args.gpus = ws if ws > 1 else args.gpus
     if args.impl == "reference":
@@ -500,6 +505,14 @@ def main():
             return layer.forward(x_dev, kv, desc, _lib.PHASE_PROMPT, 0)
     else:
         lens = lengths_for(w)
+        if ws > 1 and args.dp == "strong":
+            # batch-sharded data parallelism: the workload's
+            # sequences split over the ranks by causal cost, no collective
+            from paper_2104_12470_b200.dp import shard_lengths
+            mine = shard_lengths(lens, ws)[rank]
+            lens = [lens[i] for i in mine] or [1]
+            w["batch"] = len(lens)
+            w["dp_strong"] = True
         desc = eet.make_batch(lens)
         s = desc.seq_len
         cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=1,
@@ -548,7 +561,14 @@ def main():
         ms = float(t.item())
         dist.barrier()
     tp_mode = bool(w.get("tp"))
-    value = (1 if tp_mode else ws) * units * args.steps / (ms / 1e3)
+    strong = tp_mode or bool(w.get("dp_strong"))
+    if w.get("dp_strong"):                    # ranks hold different shards: sum of valid tokens
+        tot = torch.tensor([float(units)], device="cuda")
+        dist.all_reduce(tot)
+        units_all = tot.item()
+    else:
+        units_all = units * (1 if tp_mode else ws)
+    value = units_all * args.steps / (ms / 1e3)
 
     # end to end through the public API: host inputs in, host results out
     t0 = time.perf_counter()
@@ -560,7 +580,7 @@ def main():
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = (1 if tp_mode else ws) * units * args.steps / e2e_s
+    e2e = units_all * args.steps / e2e_s
 
     extra = {}
     if kind == "generate" and rank == 0:
@@ -649,11 +669,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if tp_mode else "weak", "vs_baseline": None,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": {"fp16": "f16", "bf16": "bf16", "fp32": "f32"}[w["dtype"]],
             "data": "synthetic (seeded random weights N(0,0.02), random token ids / hidden states)",
             "config": {"workload": w["desc"], "batch_per_gpu": w["batch"],
-                       "parallelism": f"tp{w['tp']}" if tp_mode else (f"dp{ws}" if ws > 1 else "single"),
+                       "parallelism": f"tp{w['tp']}" if tp_mode else (
+                           (f"dp{ws} batch-sharded" if w.get("dp_strong") else f"dp{ws} replicated batch")
+                           if ws > 1 else "single"),
                        "l2": "working set (weights+KV) > 126 MB L2 every step; no flush needed",
                        "tokens_per_step": units},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

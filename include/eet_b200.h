@@ -214,10 +214,16 @@ int eet_encoder_layer_forward(eet_runtime* rt, float* x, long long x_sb,
  * [4h/tp, h], w2 [h, 4h/tp]); LN parameters and x are replicated. A layer is
  *   p = attention_partial(x); all_reduce(p); residual_add(x, p);
  *   p = ffn_partial(x);       all_reduce(p); residual_add(x, p);
- * with the all-reduce (sum over ranks, fp32 [rows, h]) done by the caller's
- * communicator (NCCL over NVLink). `rows` returns the packed valid-token
- * count; partial must hold rows * h floats. The reference has no TP
- * (PAPER.md:85); these stages are new. */
+ * with the all-reduce (sum over ranks of [rows, h]) done by the caller's
+ * communicator (NCCL over NVLink). Partials are fp32 for EET_F32 and the
+ * layer dtype for EET_BF16 / EET_F16 (half the NVLink bytes). `rows`
+ * returns the packed valid-token count.
+ * Row-chunked form (the all-reduce of one chunk overlaps the GEMM of the
+ * next): attention_core (LN1, QKV, attention; context kept by the runtime)
+ * then attention_out(r0, r1) per chunk of packed rows; ffn_mid (LN2, W1,
+ * GELU; intermediate kept) then ffn_out(r0, r1); partial_rows points at row
+ * r0 of the caller's partial. The reference has no TP; these
+ * stages are new. */
 int eet_runtime_create_tp(eet_runtime** out, int dtype, int hidden,
                           int heads_total, int tp_rank, int tp_size,
                           int max_batch, int max_sequence, eet_pool* pool);
@@ -225,13 +231,24 @@ int eet_tp_attention_partial(eet_runtime* rt, const float* x, long long x_sb,
                              long long x_ss, int batch, int t,
                              const eet_layer_weights* w, void* kcache,
                              void* vcache, int kv_filled, const int* h_pads,
-                             int seq_len, int phase, float* partial, int* rows,
+                             int seq_len, int phase, void* partial, int* rows,
                              void* stream);
+int eet_tp_attention_core(eet_runtime* rt, const float* x, long long x_sb,
+                          long long x_ss, int batch, int t,
+                          const eet_layer_weights* w, void* kcache,
+                          void* vcache, int kv_filled, const int* h_pads,
+                          int seq_len, int phase, int* rows, void* stream);
+int eet_tp_attention_out(eet_runtime* rt, const eet_layer_weights* w, int r0,
+                         int r1, void* partial_rows, void* stream);
 int eet_tp_ffn_partial(eet_runtime* rt, const float* x, long long x_sb,
                        long long x_ss, const eet_layer_weights* w,
-                       float* partial, void* stream);
+                       void* partial, void* stream);
+int eet_tp_ffn_mid(eet_runtime* rt, const float* x, long long x_sb,
+                   long long x_ss, const eet_layer_weights* w, void* stream);
+int eet_tp_ffn_out(eet_runtime* rt, const eet_layer_weights* w, int r0,
+                   int r1, void* partial_rows, void* stream);
 int eet_tp_residual_add(eet_runtime* rt, float* x, long long x_sb, long long x_ss,
-                        const float* reduced, void* stream);
+                        const void* reduced, void* stream);
 
 /* ------------------------------------------------------------- generation */
 typedef struct {

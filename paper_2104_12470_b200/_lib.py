@@ -87,6 +87,10 @@ SIGNATURES = {
     "eet_runtime_create_tp": (i32, [C.POINTER(p), i32, i32, i32, i32, i32, i32, i32, p]),
     "eet_tp_attention_partial": (i32, [p, p, i64, i64, i32, i32, C.POINTER(LayerWeightsC), p, p, i32, C.POINTER(i32), i32, i32, p, C.POINTER(i32), p]),
     "eet_tp_ffn_partial": (i32, [p, p, i64, i64, C.POINTER(LayerWeightsC), p, p]),
+    "eet_tp_attention_core": (i32, [p, p, i64, i64, i32, i32, C.POINTER(LayerWeightsC), p, p, i32, C.POINTER(i32), i32, i32, C.POINTER(i32), p]),
+    "eet_tp_attention_out": (i32, [p, C.POINTER(LayerWeightsC), i32, i32, p, p]),
+    "eet_tp_ffn_mid": (i32, [p, p, i64, i64, C.POINTER(LayerWeightsC), p]),
+    "eet_tp_ffn_out": (i32, [p, C.POINTER(LayerWeightsC), i32, i32, p, p]),
     "eet_tp_residual_add": (i32, [p, p, i64, i64, p, p]),
     "eet_generate": (i32, [p, C.POINTER(ModelC), C.POINTER(i32), C.POINTER(i32), i32, i32, i32, C.POINTER(i64), p, i32, p]),
 }

@@ -140,7 +140,7 @@ void launch_argmax(const float* logits, int batch, int vocab, int* cur_tok,
                    float* logits_all, cudaStream_t st);
 void launch_advance(int* d_filled, int* d_step, cudaStream_t st);
 void launch_residual_add(float* x, long long x_sb, long long x_ss, const int2* rinfo,
-                         const float* reduced, int rows, int h, cudaStream_t st);
+                         const void* reduced, int dtype, int rows, int h, cudaStream_t st);
 
 // GEMMs (gemm_simt.cu / gemm_tc.cu). C = A[M,K] * B[N,K]^T, fp32 accumulate.
 void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M,

@@ -466,25 +466,34 @@ void launch_argmax(const float* logits, int batch, int vocab, int* cur, long lon
 }
 
 // x[valid row m] += reduced[m] : the residual add after a tensor-parallel
-// all-reduce (runtime.py:259 / :212 across shards).
+// all-reduce (runtime.py:259 / :212 across shards). The reduced partial is
+// fp32 (fp32 mode) or the layer dtype (16-bit modes: half the NVLink bytes).
+template <typename R>
 __global__ void residual_add_kernel(float* __restrict__ x, long long x_sb, long long x_ss,
-                                    const int2* __restrict__ rinfo, const float* __restrict__ r,
+                                    const int2* __restrict__ rinfo, const R* __restrict__ r,
                                     int h) {
   sm100::griddep_wait();
   sm100::griddep_launch_dependents();
   const int m = blockIdx.x;
   const int2 ri = rinfo[m];
   float* xr = x + ri.x * x_sb + ri.y * x_ss;
-  const float* rr = r + (long long)m * h;
-  for (int c = threadIdx.x; c < h; c += blockDim.x) xr[c] += rr[c];
+  const R* rr = r + (long long)m * h;
+  for (int c = threadIdx.x; c < h; c += blockDim.x) xr[c] += to_f(rr[c]);
 }
 
 void launch_residual_add(float* x, long long x_sb, long long x_ss, const int2* rinfo,
-                         const float* reduced, int rows, int h, cudaStream_t st) {
+                         const void* reduced, int dtype, int rows, int h, cudaStream_t st) {
   if (rows <= 0) return;
-  ProfScope ps(K_LAYERNORM, st, 12.0 * rows * h, 1.0 * rows * h);
-  launch_ex(residual_add_kernel, dim3(rows), dim3(256), 0, st, true, dim3(1, 1, 1), x, x_sb, x_ss,
-            rinfo, reduced, h);
+  ProfScope ps(K_LAYERNORM, st, (8.0 + dtype_size(dtype)) * rows * h, 1.0 * rows * h);
+  if (dtype == EET_F32)
+    launch_ex(residual_add_kernel<float>, dim3(rows), dim3(256), 0, st, true, dim3(1, 1, 1), x, x_sb, x_ss,
+              rinfo, reinterpret_cast<const float*>(reduced), h);
+  else if (dtype == EET_BF16)
+    launch_ex(residual_add_kernel<__nv_bfloat16>, dim3(rows), dim3(256), 0, st, true, dim3(1, 1, 1), x, x_sb,
+              x_ss, rinfo, reinterpret_cast<const __nv_bfloat16*>(reduced), h);
+  else
+    launch_ex(residual_add_kernel<__half>, dim3(rows), dim3(256), 0, st, true, dim3(1, 1, 1), x, x_sb, x_ss,
+              rinfo, reinterpret_cast<const __half*>(reduced), h);
   EET_LAUNCH_CHECK();
 }
 

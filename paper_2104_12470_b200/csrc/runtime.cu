@@ -501,6 +501,8 @@ struct eet_runtime {
   int* h_prompts = nullptr;           // pinned staging: prompts in, tokens out
   long long* h_tokens = nullptr;
   float* xdec = nullptr;              // decode residual stream [bmax, h]
+  void* tp_ctx = nullptr;             // tensor parallel: attention context kept for the row-chunked out-proj
+  void* tp_mid = nullptr;             // tensor parallel: FFN intermediate kept for the row-chunked W2
   int2* cand = nullptr;               // fused LM-head argmax candidates
   int* cand_ticket = nullptr;
   int cand_cap = 0;
@@ -566,9 +568,22 @@ static void plan_fill(StepPlan& p, int batch, int t, const int* pads, int seq, i
 // all-reduce. Cache slot of local position 0 = (kv_dev ? *kv_dev : 0) +
 // kv_base; the device form lets a captured decode step advance without
 // re-capture.
+// Tensor-parallel epilogue of the row-split projections: this rank's partial
+// sum in fp32 (fp32 mode) or the layer dtype (16-bit modes: half the bytes
+// on NVLink), rows [r0, r1) of the packed plan.
+static Epi tp_partial_epi(const eet_runtime* rt, void* partial, const float* bias) {
+  Epi e;
+  e.bias = bias;
+  e.mode = rt->dtype == EET_F32 ? EPI_STORE_F32 : EPI_STORE_T;
+  e.out = partial;
+  e.ldo = rt->h;
+  return e;
+}
+
 static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb, long long x_ss,
                        const eet_layer_weights* w, void* kc, void* vc, const int* kv_dev,
-                       int kv_base, bool causal, int L_host, float* partial, cudaStream_t st) {
+                       int kv_base, bool causal, int L_host, void* partial, cudaStream_t st,
+                       bool keep_ctx = false) {
   const int h = rt->h, hq = rt->hq, T = p.T, dt = rt->dtype;
   const size_t es = dtype_size(dt);
   const int scope = (p.phase == EET_PHASE_PROMPT) ? EET_SCOPE_WITHIN : EET_SCOPE_ACROSS;
@@ -603,7 +618,11 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     }
   }
 
-  Claim ctx(rt->pool, (size_t)T * hq * es, scope, "attention.context");
+  Claim ctx(rt->pool, keep_ctx ? 0 : (size_t)T * hq * es, scope, "attention.context");
+  if (keep_ctx) {                     // tensor parallel, row-chunked out-proj later (eet_tp_attention_out)
+    if (!rt->tp_ctx) rt->tp_ctx = rt->dev((size_t)rt->bmax * rt->smax * hq * es);
+    ctx.ptr = rt->tp_ctx;
+  }
   const float scale = 1.0f / std::sqrt((float)rt->hd);
   if (p.phase == EET_PHASE_PROMPT) {
     PrefillArgs a{};
@@ -641,13 +660,12 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     if (!skip_decode("attn")) launch_attn_decode(a, st);
   }
   q.release();
+  if (keep_ctx) return;
   {
     Epi e;
     e.bias = w->b_o;
     if (partial) {
-      e.mode = EPI_STORE_F32;
-      e.out = partial;
-      e.ldo = h;
+      e = tp_partial_epi(rt, partial, w->b_o);
     } else {
       e.mode = EPI_RESID;
       e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
@@ -665,11 +683,15 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
 // residual into x or a tensor-parallel partial as above. Both pool requests
 // use across-module scope like the reference (runtime.py:200-207).
 static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb, long long x_ss,
-                      const eet_layer_weights* w, float* partial, cudaStream_t st) {
+                      const eet_layer_weights* w, void* partial, cudaStream_t st, bool keep_mid = false) {
   const int h = rt->h, f = rt->ffn, T = p.T, dt = rt->dtype;
   const size_t es = dtype_size(dt);
   if (T == 0) return;
-  Claim mid(rt->pool, (size_t)T * f * es, EET_SCOPE_ACROSS, "ffn.intermediate");
+  Claim mid(rt->pool, keep_mid ? 0 : (size_t)T * f * es, EET_SCOPE_ACROSS, "ffn.intermediate");
+  if (keep_mid) {                     // tensor parallel, row-chunked W2 later (eet_tp_ffn_out)
+    if (!rt->tp_mid) rt->tp_mid = rt->dev((size_t)rt->bmax * rt->smax * f * es);
+    mid.ptr = rt->tp_mid;
+  }
   {
     Epi e;
     e.mode = EPI_GELU_T;
@@ -686,13 +708,12 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
       gemm(dt, ln2.ptr, h, w->w1, h, T, f, h, e, st);
     }
   }
+  if (keep_mid) return;
   {
     Epi e;
     e.bias = w->b_2;
     if (partial) {
-      e.mode = EPI_STORE_F32;
-      e.out = partial;
-      e.ldo = h;
+      e = tp_partial_epi(rt, partial, w->b_2);
     } else {
       e.mode = EPI_RESID;
       e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
@@ -837,7 +858,7 @@ static void check_layer_args(eet_runtime* rt, int batch, int t, int kv_filled, c
 int eet_tp_attention_partial(eet_runtime* rt, const float* x, long long x_sb, long long x_ss,
                              int batch, int t, const eet_layer_weights* w, void* kc, void* vc,
                              int kv_filled, const int* h_pads, int seq_len, int phase,
-                             float* partial, int* rows, void* stream) {
+                             void* partial, int* rows, void* stream) {
   EET_API_BEGIN
   check_layer_args(rt, batch, t, kv_filled, h_pads, seq_len, phase);
   StepPlan& p = rt->plans[0];
@@ -848,20 +869,68 @@ int eet_tp_attention_partial(eet_runtime* rt, const float* x, long long x_sb, lo
   EET_API_END
 }
 
+int eet_tp_attention_core(eet_runtime* rt, const float* x, long long x_sb, long long x_ss,
+                          int batch, int t, const eet_layer_weights* w, void* kc, void* vc,
+                          int kv_filled, const int* h_pads, int seq_len, int phase, int* rows, void* stream) {
+  EET_API_BEGIN
+  check_layer_args(rt, batch, t, kv_filled, h_pads, seq_len, phase);
+  StepPlan& p = rt->plans[0];
+  plan_fill(p, batch, t, h_pads, seq_len, phase, S(stream));
+  if (rows) *rows = p.T;
+  attn_block(rt, p, const_cast<float*>(x), x_sb, x_ss, w, kc, vc, nullptr, kv_filled, true,
+             kv_filled + t, nullptr, S(stream), /*keep_ctx=*/true);
+  EET_API_END
+}
+
+// row-split projection of the kept activation (ctx / mid) for packed rows
+// [r0, r1) into this rank's partial rows (ld h)
+static void tp_out_rows(eet_runtime* rt, const void* act, int K, const void* W, const float* bias, int r0,
+                        int r1, void* partial, cudaStream_t st) {
+  const StepPlan& p = rt->plans[0];
+  EET_REQUIRE(p.valid && act, EET_ERR_ARG, "tensor-parallel rows before their core stage");
+  EET_REQUIRE(r0 >= 0 && r1 <= p.T && r0 <= r1, EET_ERR_ARG, "tensor-parallel rows out of range");
+  if (r1 == r0) return;
+  const size_t es = dtype_size(rt->dtype);
+  const Epi e = tp_partial_epi(rt, partial, bias);
+  gemm(rt->dtype, reinterpret_cast<const char*>(act) + (size_t)r0 * K * es, K, W, K, r1 - r0, rt->h, K, e, st);
+}
+
+int eet_tp_attention_out(eet_runtime* rt, const eet_layer_weights* w, int r0, int r1, void* partial_rows,
+                         void* stream) {
+  EET_API_BEGIN
+  tp_out_rows(rt, rt->tp_ctx, rt->hq, w->wo, w->b_o, r0, r1, partial_rows, S(stream));
+  EET_API_END
+}
+
 int eet_tp_ffn_partial(eet_runtime* rt, const float* x, long long x_sb, long long x_ss,
-                       const eet_layer_weights* w, float* partial, void* stream) {
+                       const eet_layer_weights* w, void* partial, void* stream) {
   EET_API_BEGIN
   EET_REQUIRE(rt->plans[0].valid, EET_ERR_ARG, "ffn partial before an attention partial");
   ffn_block(rt, rt->plans[0], const_cast<float*>(x), x_sb, x_ss, w, partial, S(stream));
   EET_API_END
 }
 
+int eet_tp_ffn_mid(eet_runtime* rt, const float* x, long long x_sb, long long x_ss,
+                   const eet_layer_weights* w, void* stream) {
+  EET_API_BEGIN
+  EET_REQUIRE(rt->plans[0].valid, EET_ERR_ARG, "ffn partial before an attention partial");
+  ffn_block(rt, rt->plans[0], const_cast<float*>(x), x_sb, x_ss, w, nullptr, S(stream), /*keep_mid=*/true);
+  EET_API_END
+}
+
+int eet_tp_ffn_out(eet_runtime* rt, const eet_layer_weights* w, int r0, int r1, void* partial_rows,
+                   void* stream) {
+  EET_API_BEGIN
+  tp_out_rows(rt, rt->tp_mid, rt->ffn, w->w2, w->b_2, r0, r1, partial_rows, S(stream));
+  EET_API_END
+}
+
 int eet_tp_residual_add(eet_runtime* rt, float* x, long long x_sb, long long x_ss,
-                        const float* reduced, void* stream) {
+                        const void* reduced, void* stream) {
   EET_API_BEGIN
   EET_REQUIRE(rt->plans[0].valid, EET_ERR_ARG, "residual add before an attention partial");
   const StepPlan& p = rt->plans[0];
-  launch_residual_add(x, x_sb, x_ss, p.rinfo, reduced, p.T, rt->h, S(stream));
+  launch_residual_add(x, x_sb, x_ss, p.rinfo, reduced, rt->dtype, p.T, rt->h, S(stream));
   EET_API_END
 }
 
