@@ -440,8 +440,13 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32) attn_decode_bulk_kernel(Dec
         const uint32_t bytes = (uint32_t)(kn * hd * sizeof(T));
         T* dst = ring + buf * 2 * chunk_elems;
         sm100::mbar_expect_tx(&full[buf], 2 * bytes);
-        sm100::bulk_load(dst, Kc + (size_t)c * chunk_elems, bytes, &full[buf]);
-        sm100::bulk_load(dst + chunk_elems, Vc + (size_t)c * chunk_elems, bytes, &full[buf]);
+        if (a.kv_policy) {             // cached rows are read once per step: EVICT_FIRST
+          sm100::bulk_load_hint(dst, Kc + (size_t)c * chunk_elems, bytes, &full[buf], a.kv_policy);
+          sm100::bulk_load_hint(dst + chunk_elems, Vc + (size_t)c * chunk_elems, bytes, &full[buf], a.kv_policy);
+        } else {
+          sm100::bulk_load(dst, Kc + (size_t)c * chunk_elems, bytes, &full[buf]);
+          sm100::bulk_load(dst + chunk_elems, Vc + (size_t)c * chunk_elems, bytes, &full[buf]);
+        }
       }
     }
   } else {                                // ---- compute warps
@@ -692,8 +697,14 @@ static void decode_dispatch(const DecodeArgs& a, cudaStream_t st) {
   return decode_launch<T, 8, 32, false>(a, st);
 }
 
-void launch_attn_decode(const DecodeArgs& a, cudaStream_t st) {
-  if (a.batch <= 0) return;
+void launch_attn_decode(const DecodeArgs& a_in, cudaStream_t st) {
+  if (a_in.batch <= 0) return;
+  static const unsigned long long pol = [] {     // A/B switch: EET_DEC_KV_EVICT_FIRST=0/1
+    const char* e = std::getenv("EET_DEC_KV_EVICT_FIRST");
+    return (e && e[0] == '1') ? 0x12F0000000000000ull : 0ull;
+  }();
+  DecodeArgs a = a_in;
+  a.kv_policy = pol;
   switch (a.dtype) {
     case EET_F32: decode_dispatch<float>(a, st); break;
     case EET_BF16: decode_dispatch<__nv_bfloat16>(a, st); break;

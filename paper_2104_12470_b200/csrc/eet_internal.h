@@ -193,6 +193,7 @@ struct DecodeArgs {
   int* counters;                       // [b * heads], zero on entry, left zero
   void* o; int ldo;                    // row b
   int splits;
+  unsigned long long kv_policy = 0;    // L2 cache hint of the K/V bulk copies (0: none)
 };
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
 

@@ -208,7 +208,8 @@ __device__ __forceinline__ void dec_epi(const Epi& e, int kvs, int m, int n, flo
     } else {
       const int which = n >= 2 * e.hq;
       const int w = n - e.hq * (1 + which);
-      const int head = w / e.hd, d = w - head * e.hd;
+      const int head = (e.hd & (e.hd - 1)) ? w / e.hd : w >> (31 - __clz(e.hd));   // head_dim 64 / 128: shift
+      const int d = w - head * e.hd;
       const long long off = (((long long)m * e.heads + head) * e.smax + kvs) * e.hd + d;
       reinterpret_cast<T*>(which ? e.vc : e.kc)[off] = from_f<T>(v);
     }
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
       const int j = idx >> 5, ln_ = idx & 31;
       const int q = j * C + rank;
       float4 v = recv[(size_t)j * 32 + ln_];
-#pragma unroll 4
+#pragma unroll 2
       for (int s2 = 1; s2 < nsrc; ++s2) {
         const float4 a = recv[((size_t)s2 * per_owner + j) * 32 + ln_];
         v.x += a.x; v.y += a.y; v.z += a.z; v.w += a.w;
@@ -429,8 +430,8 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
       const int t = q / NB, nb = q - t * NB;
       const int row = t * 16 + (ln_ >> 2), tok = nb * 8 + 2 * (ln_ & 3);
       const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
+#pragma unroll 1
+      for (int i = 0; i < 4; ++i) {                    // rolled: one copy of the epilogue code
         const int n = r0 + row + 8 * (i >> 1), m = tok + (i & 1);
         if (n < sh.N && m < sh.M && !dry) dec_epi<T, MODE>(e, kvs, m, n, vv[i]);
       }

@@ -1,8 +1,8 @@
 #!/bin/bash
-# ncu evidence for profiles/: launch lists (per-launch duration, cold-cache,
-# serialised) of the c2 generate path and the c3/c4 layers, plus one
-# `--set full` capture of each dominant kernel. Run under gpurun on ONE GPU:
-#   gpurun --timeout 1800 -- 'bash tools/ncu_round.sh'
+# ncu evidence for profiles/: launch lists (per-launch duration + DRAM bytes,
+# cold-cache, serialised) of the c2 generate path and the c3/c4/c5 layers,
+# plus one `--set full` capture of each dominant kernel. ONE GPU:
+#   gpurun --timeout 2400 -- 'bash tools/ncu_round.sh'
 # Outputs land in gpurun_out/ncu/ (scratch); summaries are copied to profiles/.
 set -x
 O=gpurun_out/ncu
@@ -17,8 +17,8 @@ for w in c3 c4 c5; do
 done
 
 # full captures of the top kernels (skip the warm-up call's launches)
-timeout 600 $NCU $FULL -k regex:gemv_mma -s 300 -c 4 -o $O/gemv_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_c2.log 2>&1
-timeout 600 $NCU $FULL -k regex:gemv_tc -s 100 -c 1 -o $O/gemv_tc_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_tc_c2.log 2>&1
+timeout 600 $NCU $FULL -k regex:gemv_cl -s 400 -c 4 -o $O/gemv_cl_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_cl_c2.log 2>&1
+timeout 600 $NCU $FULL -k regex:lm_head -s 3 -c 1 -o $O/lm_head_c2 -f python tools/decode_profile.py --steps 4 > $O/lm_head_c2.log 2>&1
 timeout 600 $NCU $FULL -k regex:attn_decode -s 60 -c 2 -o $O/attn_decode_c2 -f python tools/decode_profile.py --steps 4 > $O/attn_decode_c2.log 2>&1
 timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c3 -f python tools/layer_profile.py --workload c3 > $O/attn_tc_c3.log 2>&1
 timeout 600 $NCU $FULL -k regex:gemm_tc -s 4 -c 4 -o $O/gemm_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/gemm_tc_c4.log 2>&1
@@ -27,5 +27,6 @@ ls -la $O
 # summaries on the box; the .ncu-rep files are too large to bring back
 for r in $O/*.ncu-rep; do python tools/ncu_summary.py full $r > ${r%.ncu-rep}.full.txt 2>&1; done
 for w in c2 c3 c4 c5; do python tools/ncu_summary.py launches $O/launches_$w.csv > $O/launches_$w.txt 2>&1; done
+python tools/traffic_update.py $O > $O/traffic_update.log 2>&1
 rm -f $O/*.ncu-rep
 gzip -f $O/launches_c2.csv

@@ -16,8 +16,9 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_summary  # noqa: E402
 
-KIND = [("gemm_tc", "gemm_tc"), ("attn_tc", "attn_prefill"), ("attn_decode", "attn_decode"),
-        ("gemv", "gemv"), ("ln_rows", "layernorm"), ("layernorm", "layernorm"), ("argmax", "argmax")]
+KIND = [("gemv_cl", "gemv_cl"), ("lm_head", "lm_head"), ("gemm_tc", "gemm_tc"), ("attn_tc", "attn_prefill"),
+        ("attn_decode", "attn_decode"), ("gemv", "gemv"), ("ln_rows", "layernorm"), ("layernorm", "layernorm"),
+        ("argmax", "argmax")]
 
 
 def main():
@@ -39,7 +40,7 @@ def main():
             acc[kind] = (b + d["dram_mb_per_launch"] * 1e6 * d["launches"], n + d["launches"])
         out[w] = {k: int(b / n) for k, (b, n) in acc.items()}
     out["_source"] = ("ncu launch lists (dram__bytes_read.sum + dram__bytes_write.sum per launch, mean "
-                      "over the launches of that kernel kind) in profiles/r01/ncu/; tools/ncu_round.sh, "
+                      "over the launches of that kernel kind) in profiles/r02/ncu/; tools/ncu_round.sh, "
                       "tools/traffic_update.py")
     with open(os.path.join(root, "profiles", "traffic_per_launch.json"), "w") as fh:
         json.dump(out, fh, indent=1)
