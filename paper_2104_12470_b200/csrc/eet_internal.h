@@ -156,6 +156,11 @@ void gemv_tc_sm100(int dtype, const void* A, int lda, const void* B, int ldb,
 bool gemv_tc_ln_sm100(int dtype, const float* x, long long x_sb, long long x_ss,
                       const int2* rinfo, const float* g, const float* b, const void* B,
                       int ldb, int M, int N, int K, const Epi& e, cudaStream_t st);
+// fp32 GEMM as 3xTF32 on tcgen05 (gemm_tf32.cu); false when not eligible
+bool gemm_tf32x3(const float* A, int lda, const float* B, int ldb, int M, int N, int K, const Epi& e,
+                 cudaStream_t st);
+// deterministic split-K second stage (partials summed in split order) + epilogue
+void launch_splitk_reduce(const float* part, int splits, int M, int N, const Epi& e, cudaStream_t st);
 // Dispatch by dtype and M (the one GEMM entry the runtime uses).
 void gemm(int dtype, const void* A, int lda, const void* B, int ldb, int M,
           int N, int K, const Epi& e, cudaStream_t st);

@@ -10,6 +10,7 @@
 #include "sm100.cuh"
 
 #include <algorithm>
+#include <string>
 
 namespace eet {
 
@@ -132,6 +133,14 @@ __global__ void gemm_f32_reduce_kernel(const float* __restrict__ part, int split
     for (int s = 0; s < splits; ++s) v += part[s * total + i];
     epi_apply<float>(e, (int)(i / N), (int)(i % N), v);
   }
+}
+
+void launch_splitk_reduce(const float* part, int splits, int M, int N, const Epi& e, cudaStream_t st) {
+  const long long total = (long long)M * N;
+  gemm_f32_reduce_kernel<<<(int)std::min<long long>((total + 255) / 256, 8 * device_sm_count()), 256, 0, st>>>(
+      part, splits, M, N, e);
+  count_launch();
+  EET_LAUNCH_CHECK();
 }
 
 // Split-K plan: ~2 CTAs of 256 threads per SM, >= 128 k per split. The
@@ -321,8 +330,15 @@ void gemm(int dtype, const void* A, int lda, const void* B, int ldb, int M, int 
           const Epi& e, cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
   if (dtype == EET_F32) {
-    M <= 16 ? gemv_small_m(dtype, A, lda, B, ldb, M, N, K, e, st)
-            : gemm_f32_simt((const float*)A, lda, (const float*)B, ldb, M, N, K, e, st);
+    // fp32 mode: 3xTF32 on tcgen05 (gemm_tf32.cu) for the prompt-pass
+    // projections, FFMA for decode rows and unaligned operands
+    static const bool ffma = [] {                  // A/B switch: EET_F32_GEMM=ffma
+      const char* v = std::getenv("EET_F32_GEMM");
+      return v && std::string(v) == "ffma";
+    }();
+    if (M <= 16) gemv_small_m(dtype, A, lda, B, ldb, M, N, K, e, st);
+    else if (ffma || !gemm_tf32x3(static_cast<const float*>(A), lda, static_cast<const float*>(B), ldb, M, N, K, e, st))
+      gemm_f32_simt((const float*)A, lda, (const float*)B, ldb, M, N, K, e, st);
     return;
   }
   if (tc_eligible(A, lda, B, ldb, K)) {

@@ -61,6 +61,20 @@ CUtensorMap make_tma_map_2d(const void* ptr, int rows, int K, int ld, int box_ro
   return map;
 }
 
+// fp32 K-major map: box 32 x box_rows (128-byte rows, 128B swizzle)
+CUtensorMap make_tma_map_2d_f32(const void* ptr, int rows, int K, int ld, int box_rows) {
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  EET_REQUIRE(r == CUDA_SUCCESS, EET_ERR_CUDA, "cuTensorMapEncodeTiled (fp32) failed");
+  return map;
+}
+
 // 3-D map over [planes][rows][K] with a plane pitch of plane_ld elements: a
 // box that runs past `rows` inside a plane is zero-filled instead of reading
 // the plane's tail (or the next plane).
