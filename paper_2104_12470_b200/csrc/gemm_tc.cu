@@ -61,6 +61,26 @@ CUtensorMap make_tma_map_2d(const void* ptr, int rows, int K, int ld, int box_ro
   return map;
 }
 
+// K-major 16-bit rows x K seen as [K/64 blocks][rows][64]: one box brings
+// box_rows rows x box_kblocks swizzled 128-byte column blocks (the smem
+// layout of that many box_rows x 64 2-D boxes stacked along K) in a single
+// TMA instruction
+CUtensorMap make_tma_map_kblk(const void* ptr, int rows, int K, int ld, int box_rows, int box_kblocks, int dtype) {
+  CUtensorMap map;
+  cuuint64_t dims[3] = {64u, (cuuint64_t)rows, (cuuint64_t)(K / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, 128u};
+  cuuint32_t box[3] = {64u, (cuuint32_t)box_rows, (cuuint32_t)box_kblocks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&map,
+                           dtype == EET_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                           3, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  EET_REQUIRE(r == CUDA_SUCCESS, EET_ERR_CUDA, "cuTensorMapEncodeTiled (k-blocks) failed");
+  return map;
+}
+
 // fp32 K-major map: box 32 x box_rows (128-byte rows, 128B swizzle)
 CUtensorMap make_tma_map_2d_f32(const void* ptr, int rows, int K, int ld, int box_rows) {
   CUtensorMap map;

@@ -261,8 +261,7 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapW) : "memory");
     mbar_expect_tx(wbar, (uint32_t)(R * Kc * 2));
     const uint64_t pol = 0x12F0000000000000ull;              // EVICT_FIRST: read once per step
-    for (int b = 0; b < Kc / 64; ++b)
-      tma_load_2d(smem + L.w + b * R * 128, &mapW, wbar, k0 + b * 64, r0, pol);
+    tma_load_3d(smem + L.w, &mapW, wbar, 0, r0, k0 / 64, pol);     // [Kc/64][R][64] in one box
     if (C > 1) {                                              // DSMEM arrivals (one-CTA clusters stay local)
       if (LN) mbar_expect_tx(sbar, (uint32_t)(C * 16 * 8));
       mbar_expect_tx(rbar, (uint32_t)(n_own * C * KG * 512));
@@ -478,7 +477,6 @@ __global__ void __launch_bounds__(HTHREADS) lm_head_kernel(const __grid_constant
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = (N + 15) / 16;
   const int nmine = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int kb = K / 64;
   const uint64_t pol = 0x12F0000000000000ull;
   const bool trace = g_tr_on && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1);
   long long ts[6] = {0, 0, 0, 0, 0, 0};
@@ -499,8 +497,7 @@ __global__ void __launch_bounds__(HTHREADS) lm_head_kernel(const __grid_constant
         if (i >= HSTAGES) mbar_wait(&empty[st], (uint32_t)(((i / HSTAGES) - 1) & 1));
         const int t = blockIdx.x + i * gridDim.x;
         mbar_expect_tx(&full[st], stage_bytes);
-        for (int b = 0; b < kb; ++b)
-          tma_load_2d(smem + st * stage_bytes + b * 16 * 128, &mapW, &full[st], b * 64, t * 16, pol);
+        tma_load_3d(smem + st * stage_bytes, &mapW, &full[st], 0, t * 16, 0, pol);   // 16 whole rows
         if (i + 1 == HSTAGES) {                          // static weights: the first ring fill precedes the wait
           griddep_wait();
           griddep_launch_dependents();
@@ -774,7 +771,7 @@ bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int l
   sh.early = early;
   (void)x_ss; (void)rinfo;
   const gc::LnSrc src{x, x_sb, g, b};
-  const CUtensorMap mw = make_tma_map_2d(W, N, K, K, 16 * sh.NT, dtype);
+  const CUtensorMap mw = make_tma_map_kblk(W, N, K, K, 16 * sh.NT, sh.Kc / 64, dtype);
   ProfScope ps(K_GEMV, st, (double)N * K * 2 + (double)M * K * (ln ? 4 : 2) + gemm_bytes(M, N, 0, 2, e),
                2.0 * M * N * K);
   if (dtype == EET_BF16) {
@@ -799,7 +796,7 @@ bool lm_head_argmax(int dtype, const void* W, int M, int N, int K, const float* 
   const int grid = std::min(tiles, device_sm_count());
   const size_t smem = (size_t)gc::HSTAGES * 16 * K * 2 + gc::align_up(16 * (K + gc::XPAD) * 2, 128) +
                       (size_t)gc::HCW * 16 * 8 + gc::HSTAGES * 16 + 1024 + 64;
-  const CUtensorMap mw = make_tma_map_2d(W, N, K, K, 16, dtype);
+  const CUtensorMap mw = make_tma_map_kblk(W, N, K, K, 16, K / 64, dtype);
   (void)x_ss; (void)rinfo;                       // rows: x + m * x_sb (decode plan)
   const gc::LnSrc src{x, x_sb, g, b};
   {

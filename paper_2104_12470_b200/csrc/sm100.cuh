@@ -15,6 +15,8 @@ CUtensorMap make_tma_map_2d(const void* ptr, int rows, int K, int ld, int box_ro
 // zero-filled (bounded K/V windows of the cache)
 CUtensorMap make_tma_map_3d(const void* ptr, int planes, int rows, int K, long long plane_ld,
                             int box_rows, int dtype);
+// [K/64][rows][64] view of a K-major 16-bit matrix: box = box_rows rows x box_kblocks 64-column blocks
+CUtensorMap make_tma_map_kblk(const void* ptr, int rows, int K, int ld, int box_rows, int box_kblocks, int dtype);
 // fp32 rows x K, box 32 x box_rows, 128B swizzle
 CUtensorMap make_tma_map_2d_f32(const void* ptr, int rows, int K, int ld, int box_rows);
 int device_sm_count();
