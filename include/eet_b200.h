@@ -158,6 +158,10 @@ int eet_gemv_decode(int dtype, const void* w, int N, int K, const void* X, const
  * from the step-time deltas (programmatic dependent launch intact). */
 int eet_debug_skip(const char* spec);
 
+/* Calibration: microseconds per grid-wide barrier of a persistent kernel
+ * with `ctas` CTAs (mode 0: flat arrival counter, 1: cluster-hierarchical). */
+int eet_debug_grid_barrier(int n, int ctas, int mode, float* us_per_barrier);
+
 /* Calibration: n dependent launches of an empty kernel (ctas CTAs), with or
  * without programmatic dependent launch; counter may be NULL. */
 int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream);
