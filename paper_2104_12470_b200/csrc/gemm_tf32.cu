@@ -17,8 +17,10 @@
 //               128B swizzle) into a 3-stage ring
 //   warp 1      TMEM allocator + MMA issuer (one lane): 3 x 4 MMAs of
 //               M128 N128 K8 per 32-wide k-block
-//   warps 2-5   epilogue: TMEM -> registers -> fused epilogue (or the
-//               split-K partial workspace, reduced in split order)
+//   warps 2-5   epilogue: TMEM -> registers -> fused epilogue; with split
+//               K, a partial tile in [col][row] order (coalesced stores),
+//               summed over the splits in order 0..S-1 by a wide second
+//               pass that runs the epilogue (deterministic)
 //   warps 6-9   splitters: hi / lo of the landed stage, in place (the
 //               swizzled layout is position-preserving), fence.proxy.async
 // The c1 shapes (M = 205 tokens) have 12-48 output tiles, so K is split
@@ -62,7 +64,28 @@ __device__ __forceinline__ void split4(float4& v, float4& lo) {
 
 struct Work {
   int num_m, num_n, splits, kb_per_split, nkb;
+  int dev_mode;   // development A/B (EET_TF32_DEV): 0 normal, 1 no split (1xTF32), 2 split but 1 MMA
 };
+
+// second stage: every output element sums its S partials in split order
+__global__ void __launch_bounds__(256) splitk_tiles_reduce_kernel(const float* __restrict__ part, int splits, int num_m,
+                                                                  int num_n, int M, int N, Epi e) {
+  const long long per_split = (long long)num_m * num_n * BM * BN;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < per_split; i += (long long)gridDim.x * 256) {
+    const int tile = (int)(i / (BM * BN)), idx = (int)(i % (BM * BN));
+    const int mb = tile % num_m, nb = tile / num_m;
+    const int m = mb * BM + idx % BM, n = nb * BN + idx / BM;
+    if (m >= M || n >= N) continue;
+    float p8[8];
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) p8[s2] = s2 < splits ? __ldcs(part + s2 * per_split + i) : 0.f;   // all in flight
+    float v = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) v += p8[s2];                                           // split order
+    for (int s2 = 8; s2 < splits; ++s2) v += part[s2 * per_split + i];
+    epi_apply<float>(e, m, n, v);
+  }
+}
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int M,
@@ -148,9 +171,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint32_t off = k * 32;                            // 8 tf32 = 32 bytes along K
-            mma_tf32(d_tmem, smem_desc(alo + off), smem_desc(bhi + off), idesc, (kb > kb0) | k);
-            mma_tf32(d_tmem, smem_desc(ahi + off), smem_desc(blo + off), idesc, 1);
-            mma_tf32(d_tmem, smem_desc(ahi + off), smem_desc(bhi + off), idesc, 1);
+            if (w.dev_mode == 0) {
+              mma_tf32(d_tmem, smem_desc(alo + off), smem_desc(bhi + off), idesc, (kb > kb0) | k);
+              mma_tf32(d_tmem, smem_desc(ahi + off), smem_desc(blo + off), idesc, 1);
+            }
+            mma_tf32(d_tmem, smem_desc(ahi + off), smem_desc(bhi + off), idesc, w.dev_mode ? ((kb > kb0) | k) : 1);
           }
           mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -171,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         float4* hi = reinterpret_cast<float4*>(smem + stage * STAGE_BYTES);   // A_hi, B_hi
         float4* lo = reinterpret_cast<float4*>(smem + stage * STAGE_BYTES + 2 * TILE_BYTES);
 #pragma unroll 4
-        for (int i = t; i < 2 * TILE_BYTES / 16; i += 128) {
+        for (int i = t; i < (w.dev_mode == 1 ? 0 : 2 * TILE_BYTES / 16); i += 128) {
           float4 v = hi[i], l;
           split4(v, l);
           hi[i] = v;
@@ -194,31 +219,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&tfull[as], (local >> 1) & 1);
       tc_fence_after();
       const int m = mb * BM + row;
+      const int tile = it / w.splits;
+      // split-K partial tile layout [col][row] (a warp's store = 32 consecutive rows: coalesced)
+      float* ptile = part ? part + ((size_t)sp * w.num_m * w.num_n + tile) * (BM * BN) : nullptr;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c * 32, r);
-        if (m < M) {
+        if (part) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ptile[(c * 32 + i) * BM + row] = __uint_as_float(r[i]);
+        } else if (m < M) {
           const int n0 = nb * BN + c * 32;
-          if (part) {                           // split-K: raw partial tile
-            float* dst = part + ((size_t)sp * M + m) * N;
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (n0 + i < N) dst[n0 + i] = __uint_as_float(r[i]);
-          } else {
+          for (int g = 0; g < 4; ++g) {
+            const int n = n0 + g * 8;
+            float v[8];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const int n = n0 + g * 8;
-              float v[8];
+            for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[g * 8 + i]);
+            if (n + 8 <= N) {
+              epi_apply8<float>(e, m, n, v);
+            } else {
 #pragma unroll
-              for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[g * 8 + i]);
-              if (n + 8 <= N) {
-                epi_apply8<float>(e, m, n, v);
-              } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  if (n + i < N) epi_apply<float>(e, m, n + i, v[i]);
-              }
+              for (int i = 0; i < 8; ++i)
+                if (n + i < N) epi_apply<float>(e, m, n + i, v[i]);
             }
           }
         }
@@ -253,7 +277,7 @@ bool gemm_tf32x3(const float* A, int lda, const float* B, int ldb, int M, int N,
     // per-stream workspace, grown outside graph capture (unsplit under capture if too small)
     static std::mutex mu;
     static std::unordered_map<cudaStream_t, std::pair<float*, size_t>> ws;
-    const size_t need = sizeof(float) * (size_t)splits * M * N;
+    const size_t need = sizeof(float) * (size_t)splits * num_m * num_n * BM * BN;
     std::lock_guard<std::mutex> lk(mu);
     auto& slot = ws[st];
     if (slot.second < need) {
@@ -270,7 +294,11 @@ bool gemm_tf32x3(const float* A, int lda, const float* B, int ldb, int M, int N,
     }
     if (splits > 1) part = slot.first;
   }
-  const Work w{num_m, num_n, splits, splits > 1 ? kbps : nkb, nkb};
+  static const int dev_mode = [] {               // development A/B: EET_TF32_DEV=1 (1xTF32) / 2
+    const char* v = std::getenv("EET_TF32_DEV");
+    return v ? atoi(v) : 0;
+  }();
+  const Work w{num_m, num_n, splits, splits > 1 ? kbps : nkb, nkb, dev_mode};
   const CUtensorMap ma = make_tma_map_2d_f32(A, M, K, lda, BM);
   const CUtensorMap mb = make_tma_map_2d_f32(B, N, K, ldb, BN);
   static const bool attr = [] {
@@ -283,8 +311,14 @@ bool gemm_tf32x3(const float* A, int lda, const float* B, int ldb, int M, int N,
     ProfScope ps(K_GEMM_F32, st, gemm_bytes(M, N, K, 4, e), 2.0 * M * N * K);
     gemm_tf32x3_kernel<<<std::min(items, sms), THREADS, SMEM, st>>>(ma, mb, M, N, K, e, w, part);
     EET_LAUNCH_CHECK();
+    if (part) {                             // the reduce pass is part of the GEMM's measured time
+      const long long per_split = (long long)num_m * num_n * BM * BN;
+      splitk_tiles_reduce_kernel<<<(int)std::min<long long>((per_split + 255) / 256, 4LL * sms), 256, 0, st>>>(
+          part, splits, num_m, num_n, M, N, e);
+      count_launch();
+      EET_LAUNCH_CHECK();
+    }
   }
-  if (part) launch_splitk_reduce(part, splits, M, N, e, st);
   return true;
 }
 

@@ -238,20 +238,20 @@ def _ptr(t) -> int | None:
 def _fingerprint(arrays) -> tuple:
     """Identity + version of the source arrays behind a cached device upload:
     object id and shape of every array, torch's in-place version counter for
-    tensors, and 8 strided samples of every numpy array (an in-place write
-    that touches none of them goes unseen: call ``invalidate_device_cache``
-    after editing weights in place)."""
+    tensors, and 4 sampled elements of every numpy array (first, thirds,
+    last; an in-place write that touches none of them goes unseen: call
+    ``invalidate_device_cache`` after editing weights in place). ~1 us per
+    array: it runs on every forward."""
     fp = []
     for a in arrays:
         if a is None:
             fp.append(None)
             continue
-        if _is_dev(a) or hasattr(a, "_version"):
+        if hasattr(a, "_version"):                       # torch tensor
             fp.append((id(a), tuple(a.shape), int(a._version)))
             continue
-        flat = np.asarray(a).reshape(-1)
-        step = max(1, flat.size // 8)
-        fp.append((id(a), flat.shape, flat[::step][:8].tobytes()))
+        n = a.size
+        fp.append((id(a), a.shape) + ((a.item(0), a.item(n // 3), a.item(2 * n // 3), a.item(n - 1)) if n else ()))
     return tuple(fp)
 
 
