@@ -11,12 +11,18 @@
 //   warp 8      TMA producer: Q_A, Q_B once, then K/V tiles (64 keys) into a
 //               two-stage ring straight from the [b, heads, s_max, hd] cache
 //   warp 9      TMEM allocator + MMA issuer: S_X = Q_X K_j^T (M128 N64) and
-//               O_X += P_X V_j (M128 N=hd; P K-major from smem, V MN-major)
+//               O_X += P_X V_j (M128 N=hd; P read from TMEM, V MN-major)
+//
+// P goes through TMEM (default; EET_ATTN_PTMEM=0 keeps the smem path): the
+// softmax writes P (16-bit pairs) over the S buffer it has just read and the
+// PV MMA takes its A operand from TMEM. The 64 KB of smem P buffers this
+// frees become K/V ring stages (5 at head_dim 128, 7 at 64): r02, c4
+// attention 1.78 -> 1.49 ms, c5 215 -> 187 us, c3 119 -> 109 us.
 //
 // O accumulates in TMEM across key tiles; a softmax thread rescales its O
 // row (tcgen05.ld/st) only when its running max grows by more than 2^8
 // (lazy rescaling), so the common tile costs one TMEM read of S and one
-// smem write of P per row. With two query tiles the tensor core works on
+// TMEM write of P per row. With two query tiles the tensor core works on
 // one tile while the softmax warps of the other run.
 #include "sm100.cuh"
 
@@ -45,10 +51,26 @@ template <int HD> struct Cfg {
   static constexpr int P_BYTES = BQ * BKV * 2;          // 128 queries x 64 keys, one atom wide
   // P double-buffered per tile: softmax(j+1) writes while PV(j) reads
   static constexpr int SMEM = 2 * Q_BYTES + 2 * NST * KV_BYTES + 4 * P_BYTES + 1024 + 256;
+  // P through TMEM: no P buffers in smem, the space goes to K/V stages
+  static constexpr int NST_PT = (2 * NST * KV_BYTES + 4 * P_BYTES) / (2 * KV_BYTES);
+  static constexpr int SMEM_PT = 2 * Q_BYTES + 2 * NST_PT * KV_BYTES + 1024 + 256;
   // TMEM columns: S_A | S_B | O_A | O_B
   // TMEM columns: S_A[2] | S_B[2] (double-buffered scores) | O_A | O_B
   static constexpr uint32_t S_COL = 0, O_COL = 4 * BKV;
 };
+
+// tcgen05.mma with the A operand (P, 128 lanes x 16 keys as 8 packed
+// 32-bit columns) read from TMEM: the softmax writes P over the S buffer it
+// has just consumed, so P never round-trips through shared memory
+__device__ __forceinline__ void mma_f16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accum));
+}
 
 // V is read MN-major: 8-key row groups 1024 B apart (SBO), 64-wide hd blocks
 // one sub-tile apart (LBO).
@@ -160,6 +182,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// tcgen05.st 32 lanes x 4 columns, no wait (the caller waits once)
+__device__ __forceinline__ void tmem_st4_nowait(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+
 struct FaArgs {
   const int* pads;          // [b]
   const int* q_rowbase;     // packed row of slot s = q_rowbase[b] + s
@@ -167,6 +196,7 @@ struct FaArgs {
   int batch, seq, heads, smax, causal;
   float scale_log2;         // (1/sqrt(hd)) * log2(e)
   int poly;                 // polynomial exp2 for half of the keys of full tiles
+  int p_tmem;               // P through TMEM (over the spent S buffer) instead of smem
   int nitems;               // > 0: persistent CTAs walk the work list
   int* ctr;                 // [2] next list entry, CTAs done (zero between launches)
 };
@@ -181,7 +211,7 @@ struct FaItems {
   uint32_t v[MAX_ITEMS];                        // b << 16 | head << 8 | pair
 };
 
-template <typename T, int HD>
+template <typename T, int HD, bool PT>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
                    const __grid_constant__ CUtensorMap mapV, FaArgs a,
@@ -222,14 +252,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (!decode(0, w0)) return;
   }
 
+  constexpr int NST = PT ? C::NST_PT : fa::NST;           // K/V ring stages
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   uint8_t* sQ = sm;                                       // [2] query tiles
   uint8_t* sK = sQ + 2 * C::Q_BYTES;                      // [NST] stages
   uint8_t* sV = sK + NST * C::KV_BYTES;                   // [NST] stages
-  uint8_t* sP = sV + NST * C::KV_BYTES;                   // [2] tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * C::P_BYTES);     // sP: [2 tiles][2 buffers]
+  uint8_t* sP = sV + NST * C::KV_BYTES;                   // [2] tiles (smem-P instance only)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(PT ? sP : sP + 4 * C::P_BYTES);     // sP: [2 tiles][2 buffers]
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;              // [NST]
   uint64_t* kv_empty = bars + 1 + NST;       // [NST]
@@ -342,12 +373,21 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int c = (t ? cB : cA) + j;
           mbar_wait(&p_full[t * 2 + (c & 1)], (c >> 1) & 1);
           tc_fence_after();
-          const uint32_t p_base = smem_u32(sP + (t * 2 + (c & 1)) * C::P_BYTES);
           const uint32_t v_base = smem_u32(sV + ((g0 + j) % NST) * C::KV_BYTES);
+          if (PT) {
+            // P(j) sits in the first BKV/2 columns of S_t buffer (c & 1)
+            const uint32_t p_tm = tmem + C::S_COL + (t * 2 + (c & 1)) * BKV;
 #pragma unroll
-          for (int k = 0; k < BKV / 16; ++k)
-            mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
-                    smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
+            for (int k = 0; k < BKV / 16; ++k)
+              mma_f16_ta(tmem + C::O_COL + t * HD, p_tm + k * 8, smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o,
+                         (j > 0) | k);
+          } else {
+            const uint32_t p_base = smem_u32(sP + (t * 2 + (c & 1)) * C::P_BYTES);
+#pragma unroll
+            for (int k = 0; k < BKV / 16; ++k)
+              mma_f16(tmem + C::O_COL + t * HD, smem_desc(p_base + k * 32),
+                      smem_desc_mn(v_base + k * 2048, C::KVSUB), id_o, (j > 0) | k);
+          }
           mma_commit(&o_done[t * 2 + (c & 1)]);
         };
         int kv_seen = -1;
@@ -450,7 +490,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       tmax *= a.scale_log2;                               // scale > 0: max commutes
       // P buffer j & 1 was last read by PV(j-2)
       uint8_t* prow = prow0 + (c & 1) * C::P_BYTES;
-      if (c >= 2) mbar_wait(&o_done[t * 2 + (c & 1)], ((c - 2) >> 1) & 1);
+      // smem P: buffer c & 1 was last read by PV(c - 2). TMEM P overwrites
+      // the S buffer just read; S(c + 2) into it is issued after PV(c)
+      // (tcgen05 MMAs of one thread execute in order)
+      if (!PT && c >= 2) mbar_wait(&o_done[t * 2 + (c & 1)], ((c - 2) >> 1) & 1);
       tc_fence_after();
       // tcgen05.ld/st are .sync.aligned: the O rescale is decided per warp
       // (any row whose max grew past the threshold rescales the whole warp;
@@ -504,7 +547,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             f2unpack(p2, p0, p1);
             pk[i >> 1] = pack2(p0, p1, BF);
           }
-          *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          if (PT) tmem_st4_nowait(s_addr + c * 4, pk);    // 8 keys = 4 packed columns
+          else *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
         const uint64_t rs2 = fadd2(fadd2(rs2v[0], rs2v[1]), fadd2(rs2v[2], rs2v[3]));
         float r0, r1;
@@ -521,11 +565,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             rs += p0 + p1;
             pk[i >> 1] = pack2(p0, p1, BF);
           }
-          *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          if (PT) tmem_st4_nowait(s_addr + c * 4, pk);
+          else *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
       }
       l += rs;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
+      if (PT) {
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");   // P over the spent S buffer
+      } else {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // P -> tensor core
+      }
       tc_fence_before();
       mbar_arrive(&p_full[t * 2 + (c & 1)]);
     }
@@ -593,9 +642,17 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
     return e ? atoi(e) : 1;
   }();
   a.poly = poly;
-  auto kern = attn_tc_kernel<T, HD>;
-  static const bool attr = [&] {                     // thread-safe one-time init
-    EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  static const int p_tmem = [] {          // A/B switch: EET_ATTN_PTMEM=0 -> P through smem
+    const char* e = std::getenv("EET_ATTN_PTMEM");
+    return e ? atoi(e) : 1;
+  }();
+  a.p_tmem = p_tmem;
+  auto kern = a.p_tmem ? attn_tc_kernel<T, HD, true> : attn_tc_kernel<T, HD, false>;
+  static const bool attr = [] {                      // thread-safe one-time init (both instances)
+    EET_CHECK_CUDA(cudaFuncSetAttribute(attn_tc_kernel<T, HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        C::SMEM_PT));
+    EET_CHECK_CUDA(cudaFuncSetAttribute(attn_tc_kernel<T, HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        C::SMEM));
     return true;
   }();
   (void)attr;
@@ -679,7 +736,7 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   dim3 grid = a.nitems > 0 ? dim3((unsigned)std::min(a.nitems, device_sm_count()), 1, 1)
                            : dim3(npair, p.heads, p.batch);
   ProfScope ps(K_ATTN_PREFILL, st, bytes, flops);
-  kern<<<grid, THREADS, C::SMEM, st>>>(mq, mk, mv, a, items);
+  kern<<<grid, THREADS, a.p_tmem ? C::SMEM_PT : C::SMEM, st>>>(mq, mk, mv, a, items);
   EET_LAUNCH_CHECK();
 }
 

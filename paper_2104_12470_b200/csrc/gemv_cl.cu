@@ -764,11 +764,11 @@ bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int l
     return (v && v[0] == '1') ? 1 : 0;
   }();
   sh.warm = warm;
-  static const int early = [] {                    // A/B switch: EET_PDL_EARLY=1
+  static const int early = [] {                    // A/B switch: EET_PDL_EARLY=1 (all) / 2 (QKV)
     const char* v = std::getenv("EET_PDL_EARLY");
-    return (v && v[0] == '1') ? 1 : 0;
+    return v ? atoi(v) : 0;
   }();
-  sh.early = early;
+  sh.early = early == 1 || (early == 2 && e.mode == EPI_QKV);   // 2: only QKV (its attention streams K/V early)
   (void)x_ss; (void)rinfo;
   const gc::LnSrc src{x, x_sb, g, b};
   const CUtensorMap mw = make_tma_map_kblk(W, N, K, K, 16 * sh.NT, sh.Kc / 64, dtype);
