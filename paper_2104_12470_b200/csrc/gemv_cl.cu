@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
 // 16-row vocab tiles (full K, no cross-warp reduction) from an HSTAGES TMA
 // ring filled by one producer warp; every consumer keeps a running
 // (max, lowest id) per token in registers.
-constexpr int HSTAGES = 5, HCW = 4, HTHREADS = (HCW + 1) * 32;
+constexpr int HSTAGES = 6, HCW = 4, HTHREADS = (HCW + 1) * 32;   // 6 x 32 KB stages + 33 KB token rows
 
 __device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
   return v > bv || (v == bv && i < bi);
