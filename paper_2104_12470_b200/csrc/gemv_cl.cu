@@ -664,9 +664,13 @@ __global__ void __launch_bounds__(256) argmax_cand_kernel(const int2* __restrict
 static bool plan(int M, int N, int K, int NB, Shape& sh, size_t& smem) {
   if (M < 1 || M > 16 || N < 1 || K % 64) return false;
   const int sms = device_sm_count();
+  static const int c_max = [] {                  // A/B switch: EET_CL_C = largest cluster size tried
+    const char* v = std::getenv("EET_CL_C");
+    return v ? std::max(1, std::min(16, atoi(v))) : 8;
+  }();
   int C = 0;
-  for (int c : {8, 6, 4, 3, 2, 1})
-    if (K % (64 * c) == 0 && K / c <= MAX_KC) { C = c; break; }
+  for (int c : {16, 8, 6, 4, 3, 2, 1})
+    if (c <= c_max && K % (64 * c) == 0 && K / c <= MAX_KC) { C = c; break; }
   if (!C) return false;
   const int Kc = K / C, KS = Kc / 16;
   const int tiles = (N + 15) / 16;
@@ -694,6 +698,7 @@ static void launch(const CUtensorMap& mw, const LnSrc& ln, const Shape& sh, size
   auto kern = gemv_cl_kernel<T, NB, NV, MODE, TRACE>;
   static std::atomic<size_t> set{0};
   if (set.load() < smem) {
+    EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));   // C = 16 (A/B)
     EET_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     size_t cur = set.load();
     while (cur < smem && !set.compare_exchange_weak(cur, smem)) {}
