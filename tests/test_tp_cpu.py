@@ -86,3 +86,21 @@ def test_shard_shapes_and_config():
     cfg = eet.ModelConfig(2, 96, 1, 12, 8, 16)
     sc = shard_config(cfg, 4)
     assert (sc.head_count, sc.head_dim) == (3, 8)
+
+
+def test_row_chunks_cover_rows_in_whole_tiles():
+    """TensorParallelLayer._chunks: the row-chunked out-proj / W2 (each chunk
+    all-reduced while the next one's GEMM runs) covers [0, rows) exactly,
+    in order, with chunk boundaries on whole 128-row GEMM tiles."""
+    from paper_2104_12470_b200.tp import TensorParallelLayer
+    layer = TensorParallelLayer.__new__(TensorParallelLayer)
+    for chunks in (0, 1, 3, 4):
+        layer.chunks = chunks
+        for rows in (1, 100, 128, 255, 256, 1000, 1024, 2048, 15133):
+            parts = layer._chunks(rows)
+            assert parts[0][0] == 0 and parts[-1][1] == rows
+            for (a, b), (c, _) in zip(parts, parts[1:]):
+                assert b == c and b % 128 == 0
+            assert all(b > a for a, b in parts)
+            if chunks:
+                assert len(parts) <= chunks
