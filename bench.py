@@ -52,7 +52,8 @@ WORKLOADS = {
                max_seq=1024, dtype="fp16", batch=16,
                desc="GPT-2 medium (h1024, 24L, 16 heads, V50257), prompt 512 + greedy 512, fp16"),
     "c1": dict(hidden=768, layers=1, heads=12, batch=4, prompt=64, dtype="fp32", kind="layer",
-               lengths="ratio0.2", desc="decoder layer h768 12 heads b4 s64 (pad 0.2), fp32"),
+               lengths="ratio0.2", padding_side="right",
+               desc="decoder layer h768 12 heads b4 s64, right-padded (pad ratio 0.2), fp32"),
     "c3": dict(hidden=2048, layers=1, heads=16, batch=32, prompt=1024, dtype="bf16", kind="layer",
                lengths="ragged3", desc="decoder layer h2048 16 heads s1024 b32 ragged, bf16"),
     "c4": dict(hidden=4096, layers=1, heads=32, batch=8, prompt=4096, dtype="bf16", kind="layer",
@@ -513,7 +514,9 @@ def main():
             lens = [lens[i] for i in mine] or [1]
             w["batch"] = len(lens)
             w["dp_strong"] = True
-        desc = eet.make_batch(lens)
+        # BASELINE configs[0] (c1) is right-padded: native valid windows [0, len_b)
+        side = w.get("padding_side", "left")
+        desc = eet.make_batch(lens, padding_side=side)
         s = desc.seq_len
         cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=1,
                               head_count=w["heads"], max_prompt=s, max_sequence=s,

@@ -206,6 +206,23 @@ int eet_decoder_layer_forward(eet_runtime* rt, float* x, long long x_sb,
                               void* vcache, int kv_filled, const int* h_pads,
                               int seq_len, int phase, void* stream);
 
+/* Windowed prompt pass (new; SURVEY App. B.1 — the reference is left-pad
+ * only): sequence b's valid slots are [h_start[b], h_end[b]) of the t-slot
+ * rows of x, e.g. right padding = start 0, end len_b. Same layout, cache and
+ * kernels as eet_decoder_layer_forward with phase PROMPT (kv cursor 0); slots
+ * outside the window are skipped, not masked, and K/V is written only for
+ * the window. Incremental steps need one common cursor: left-pad batches. */
+int eet_decoder_layer_forward_window(eet_runtime* rt, float* x, long long x_sb,
+                                     long long x_ss, int batch, int t,
+                                     const eet_layer_weights* w, void* kcache,
+                                     void* vcache, const int* h_start,
+                                     const int* h_end, void* stream);
+int eet_encoder_layer_forward_window(eet_runtime* rt, float* x, long long x_sb,
+                                     long long x_ss, int batch, int t,
+                                     const eet_layer_weights* w,
+                                     const int* h_start, const int* h_end,
+                                     void* stream);
+
 /* encoder_layer_forward (runtime.py:266-301): bidirectional, no cache. */
 int eet_encoder_layer_forward(eet_runtime* rt, float* x, long long x_sb,
                               long long x_ss, int batch, int t,

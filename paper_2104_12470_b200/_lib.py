@@ -85,6 +85,8 @@ SIGNATURES = {
     "eet_runtime_destroy": (i32, [p]),
     "eet_decoder_layer_forward": (i32, [p, p, i64, i64, i32, i32, C.POINTER(LayerWeightsC), p, p, i32, C.POINTER(i32), i32, i32, p]),
     "eet_encoder_layer_forward": (i32, [p, p, i64, i64, i32, i32, C.POINTER(LayerWeightsC), C.POINTER(i32), p]),
+    "eet_decoder_layer_forward_window": (i32, [p, p, i64, i64, i32, i32, C.POINTER(LayerWeightsC), p, p, C.POINTER(i32), C.POINTER(i32), p]),
+    "eet_encoder_layer_forward_window": (i32, [p, p, i64, i64, i32, i32, C.POINTER(LayerWeightsC), C.POINTER(i32), C.POINTER(i32), p]),
     "eet_runtime_create_tp": (i32, [C.POINTER(p), i32, i32, i32, i32, i32, i32, i32, p]),
     "eet_tp_attention_partial": (i32, [p, p, i64, i64, i32, i32, C.POINTER(LayerWeightsC), p, p, i32, C.POINTER(i32), i32, i32, p, C.POINTER(i32), p]),
     "eet_tp_ffn_partial": (i32, [p, p, i64, i64, C.POINTER(LayerWeightsC), p, p]),

@@ -94,12 +94,17 @@ def validate_config(cfg: ModelConfig) -> ModelConfig:
 
 @dataclass(frozen=True)
 class BatchDescriptor:
-    """Left-padded uneven batch: sequence i's pads occupy [0, padding_len[i])
-    (core.py:98-123)."""
+    """Uneven batch (core.py:98-123): left-padded as in the reference —
+    sequence i's pads occupy [0, padding_len[i]) — or, new here
+    (``padding_side="right"``, BASELINE c1), right-padded:
+    its pads occupy [seq_len - padding_len[i], seq_len). A right-padded batch
+    runs the prompt pass natively (valid windows, nothing re-laid); the
+    incremental phase needs the reference's left padding."""
 
     seq_len: int
     padding_len: tuple
     batch: int
+    padding_side: str = "left"
 
     def __post_init__(self):
         if self.batch < 1:
@@ -110,13 +115,22 @@ class BatchDescriptor:
         if bad:
             i = bad[0]
             raise ValueError(f"padding_len[{i}]={self.padding_len[i]} outside [0, {self.seq_len})")
+        if self.padding_side not in ("left", "right"):
+            raise ValueError(f"padding_side must be 'left' or 'right', got {self.padding_side!r}")
 
     def pads_array(self) -> np.ndarray:
         return np.asarray(self.padding_len, dtype=np.int32)
 
+    def windows(self):
+        """(start, end) of every sequence's valid slots."""
+        if self.padding_side == "right":
+            return [(0, self.seq_len - p) for p in self.padding_len]
+        return [(p, self.seq_len) for p in self.padding_len]
 
-def make_batch(prompt_lengths, target_len: int | None = None) -> BatchDescriptor:
-    """Max-length strategy (core.py:126-146): pad every prompt on the left to
+
+def make_batch(prompt_lengths, target_len: int | None = None, padding_side: str = "left") -> BatchDescriptor:
+    """Max-length strategy (core.py:126-146): pad every prompt on the left
+    (the reference) or, with ``padding_side="right"``, on the right, to
     ``target_len`` (default: the longest prompt)."""
     lengths = [int(n) for n in prompt_lengths]
     if not lengths:
@@ -127,4 +141,4 @@ def make_batch(prompt_lengths, target_len: int | None = None) -> BatchDescriptor
     if target < max(lengths):
         raise ValueError(f"target_len {target} shorter than longest prompt {max(lengths)}")
     return BatchDescriptor(seq_len=target, padding_len=tuple(target - n for n in lengths),
-                           batch=len(lengths))
+                           batch=len(lengths), padding_side=padding_side)

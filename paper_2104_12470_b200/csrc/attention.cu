@@ -30,15 +30,16 @@ __global__ void __launch_bounds__(PTHREADS) attn_prefill_kernel(PrefillArgs a) {
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int b = blockIdx.z, head = blockIdx.y, q0 = blockIdx.x * PQ;
   const int pad = a.pads[b];
-  const int seq = a.seq, hd = a.hd;
+  // valid slots [pad, seq): seq = this sequence's end (right-padded windows) or the common length
+  const int seq = a.ends ? a.ends[b] : a.seq, hd = a.hd;
   const int qhi = min(q0 + PQ, seq);
   const T* Q = reinterpret_cast<const T*>(a.q);
   const T* K = reinterpret_cast<const T*>(a.k);
   const T* V = reinterpret_cast<const T*>(a.v);
   T* O = reinterpret_cast<T*>(a.o);
   // packed layouts give a per-sequence row base; padded layouts use b * seq
-  const long long qrb = a.q_rowbase ? a.q_rowbase[b] : (long long)b * seq;
-  const long long orb = a.o_rowbase ? a.o_rowbase[b] : (long long)b * seq;
+  const long long qrb = a.q_rowbase ? a.q_rowbase[b] : (long long)b * a.seq;
+  const long long orb = a.o_rowbase ? a.o_rowbase[b] : (long long)b * a.seq;
 
   if (a.zero_pad_rows) {                   // padded layout: pad-query rows are exact zeros
     int zend = min(pad, qhi);
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(PTHREADS) attn_prefill_kernel(PrefillArgs a) {
       O[(orb + r) * a.ldo + head * hd + d] = from_f<T>(0.f);
     }
   }
-  if (qhi <= pad) return;                  // whole tile is padding: skipped
+  if (qhi <= pad || q0 >= seq) return;    // whole tile is padding: skipped
 
   // Q tile (rows outside [pad, seq) and dims >= hd are zero)
   for (int idx = tid; idx < PQ * HD; idx += PTHREADS) {
@@ -186,12 +187,36 @@ static void prefill_dispatch(const PrefillArgs& a, cudaStream_t st, double bytes
   else EET_REQUIRE(false, EET_ERR_UNSUPPORTED, "attention: head_dim > 128 not supported");
 }
 
+// Right-padded / windowed prompt pass on the tensor-core path: the last
+// 64-key K/V tile of sequence b may reach past its end into cache slots this
+// pass never wrote (stale values, possibly NaN); their P is 0 but 0 * NaN is
+// NaN in the PV MMA. Zero those slots [end_b, min(seq, pad_b + 64 *
+// ceil((end_b - pad_b) / 64))) of every (b, head) plane first.
+__global__ void kv_zero_tail_kernel(PrefillArgs a, int es) {
+  const int b = blockIdx.y, head = blockIdx.x;
+  const int pad = a.pads[b], end = a.ends[b];
+  const int tail = min(a.seq, pad + ((end - pad + 63) / 64) * 64);
+  const long long row_bytes = (long long)a.hd * es;
+  char* kb = reinterpret_cast<char*>(const_cast<void*>(a.k)) + ((long long)b * a.k_sb + (long long)head * a.k_sh) * es;
+  char* vb = reinterpret_cast<char*>(const_cast<void*>(a.v)) + ((long long)b * a.k_sb + (long long)head * a.k_sh) * es;
+  const long long n = (long long)(tail - end) * row_bytes / 4;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    reinterpret_cast<int*>(kb + end * row_bytes)[i] = 0;
+    reinterpret_cast<int*>(vb + end * row_bytes)[i] = 0;
+  }
+}
+
 void launch_attn_prefill(const PrefillArgs& a, cudaStream_t st) {
   if (a.batch <= 0 || a.seq <= 0) return;
+  if (a.ends && a.dtype != EET_F32 && a.k_ss == a.hd) {
+    kv_zero_tail_kernel<<<dim3(a.heads, a.batch), 128, 0, st>>>(a, (int)dtype_size(a.dtype));
+    count_launch();
+    EET_LAUNCH_CHECK();
+  }
   // algorithmic work: valid (query, key) pairs only (pads skipped)
   double pairs = 0, rows = 0;
   for (int b = 0; b < a.batch && a.h_pads; ++b) {
-    double len = a.seq - a.h_pads[b];
+    double len = (a.h_ends ? a.h_ends[b] : a.seq) - a.h_pads[b];
     pairs += a.causal ? len * (len + 1) / 2 : len * len;
     rows += len;
   }

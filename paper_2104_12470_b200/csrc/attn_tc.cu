@@ -199,6 +199,7 @@ struct FaArgs {
   int p_tmem;               // P through TMEM (over the spent S buffer) instead of smem
   int nitems;               // > 0: persistent CTAs walk the work list
   int* ctr;                 // [2] next list entry, CTAs done (zero between launches)
+  const int* ends;          // [b] valid end per sequence (windows), nullptr: seq
 };
 
 // Work list: one entry per non-empty (sequence, head, query-tile pair),
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   // from a global counter (greedy, in list order); without one, the CTA runs
   // the single (pair, head, b) of its block index.
   const int n_work = a.nitems;
-  struct Item { int b, head, q0, pad, ntA, ntB; };
+  struct Item { int b, head, q0, pad, end, ntA, ntB; };
   auto decode = [&](int lin, Item& w) -> bool {
     int pair;
     if (n_work > 0) {
@@ -239,10 +240,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     w.q0 = pair * 2 * BQ;
     w.pad = a.pads[w.b];
-    const int qhiA = min(w.q0 + BQ, a.seq), qhiB = min(w.q0 + 2 * BQ, a.seq);
-    if (qhiB <= w.pad) return false;                      // both tiles in the padding
-    const bool liveA = qhiA > w.pad && w.q0 < a.seq;
-    const int kendA = a.causal ? qhiA : a.seq, kendB = a.causal ? qhiB : a.seq;
+    w.end = a.ends ? a.ends[w.b] : a.seq;                 // valid slots [pad, end)
+    const int qhiA = min(w.q0 + BQ, w.end), qhiB = min(w.q0 + 2 * BQ, w.end);
+    if (qhiB <= w.pad || w.q0 >= w.end) return false;     // both tiles in the padding
+    const bool liveA = qhiA > w.pad && w.q0 < w.end;
+    const int kendA = a.causal ? qhiA : w.end, kendB = a.causal ? qhiB : w.end;
     w.ntA = liveA ? (kendA - w.pad + BKV - 1) / BKV : 0;
     w.ntB = (kendB - w.pad + BKV - 1) / BKV;              // B's range covers A's
     return true;
@@ -447,8 +449,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int pad = w.pad;
     const int qs = w.q0 + t * BQ + row;
     const int ntile = t == 0 ? w.ntA : w.ntB;
-    const bool live = qs >= pad && qs < a.seq;
-    const int row_kend = live ? (a.causal ? qs + 1 : a.seq) : pad;   // keys [pad, row_kend)
+    const bool live = qs >= pad && qs < w.end;
+    const int row_kend = live ? (a.causal ? qs + 1 : w.end) : pad;   // keys [pad, row_kend)
     float m = -INFINITY, l = 0.f;                         // m in log2 units (scaled)
     for (int j = 0; j < ntile; ++j) {
       const int c = cb + j;
@@ -633,6 +635,7 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   a.ldo = p.ldo;
   a.batch = p.batch;
   a.seq = p.seq;
+  a.ends = p.ends;
   a.heads = p.heads;
   a.smax = (int)(p.k_sh / p.hd);
   a.causal = p.causal;
@@ -662,16 +665,20 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
   a.ctr = nullptr;
   static const bool no_list = std::getenv("EET_ATTN_GRID") != nullptr;   // A/B switch
   if (p.h_pads && !no_list && npair <= 256 && p.heads <= 256 && p.batch <= 65536) {
+    auto end_of = [&](int b) { return p.h_ends ? p.h_ends[b] : p.seq; };   // valid slots [pad, end)
+    auto live_pair = [&](int b, int pr) {
+      return pr * 2 * BQ < end_of(b) && std::min((pr + 1) * 2 * BQ, end_of(b)) > p.h_pads[b];
+    };
     thread_local std::vector<int> order;
     order.resize(p.batch);
     for (int b = 0; b < p.batch; ++b) order[b] = b;
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return p.h_pads[x] < p.h_pads[y]; });
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return end_of(x) - p.h_pads[x] > end_of(y) - p.h_pads[y]; });
     long long n = 0;
     for (int b : order) {
-      const int pad = p.h_pads[b];
-      int pairs = 0;                                    // non-empty pairs: qhiB > pad
+      int pairs = 0;                                    // non-empty pairs
       for (int pr = npair - 1; pr >= 0; --pr)
-        if (std::min((pr + 1) * 2 * BQ, p.seq) > pad) ++pairs;
+        if (live_pair(b, pr)) ++pairs;
       n += (long long)pairs * p.heads;
     }
     if (n <= MAX_ITEMS) {
@@ -684,20 +691,21 @@ static void launch(const PrefillArgs& p, int T_rows, cudaStream_t st, double byt
       }();
       int maxc = 1;
       auto cost = [&](int b, int pr) {
-        const int pad = p.h_pads[b], q0 = pr * 2 * BQ;
-        const int qhiA = std::min(q0 + BQ, p.seq), qhiB = std::min(q0 + 2 * BQ, p.seq);
-        const bool liveA = qhiA > pad && q0 < p.seq;
-        const int kA = p.causal ? qhiA : p.seq, kB = p.causal ? qhiB : p.seq;
+        const int pad = p.h_pads[b], q0 = pr * 2 * BQ, end = end_of(b);
+        const int qhiA = std::min(q0 + BQ, end), qhiB = std::min(q0 + 2 * BQ, end);
+        const bool liveA = qhiA > pad && q0 < end;
+        const int kA = p.causal ? qhiA : end, kB = p.causal ? qhiB : end;
         return (liveA ? (kA - pad + BKV - 1) / BKV : 0) + (kB - pad + BKV - 1) / BKV;
       };
       for (int b = 0; b < p.batch; ++b)
-        if (p.h_pads[b] < p.seq) maxc = std::max(maxc, cost(b, npair - 1));
+        for (int pr = npair - 1; pr >= 0; --pr)
+          if (live_pair(b, pr)) { maxc = std::max(maxc, cost(b, pr)); break; }
       thread_local std::vector<std::pair<int, uint32_t>> work;
       work.clear();
       for (int b : order)
         for (int h = 0; h < p.heads; ++h)
           for (int pr = npair - 1; pr >= 0; --pr)
-            if (std::min((pr + 1) * 2 * BQ, p.seq) > p.h_pads[b]) {
+            if (live_pair(b, pr)) {
               const int c = cost(b, pr);
               const int phase = nb_env > 0 ? (int)((long long)(maxc - c) * nb_env / (maxc + 1)) : maxc - c;
               work.emplace_back(phase, ((uint32_t)b << 16) | ((uint32_t)h << 8) | (uint32_t)pr);

@@ -179,6 +179,8 @@ struct PrefillArgs {
   int causal;
   int zero_pad_rows;   // padded layout: write zero rows for pad queries
   int q_rows;          // rows of the packed q buffer (TMA extent)
+  const int* ends = nullptr;     // [b] valid end per sequence (windows); nullptr: seq
+  const int* h_ends = nullptr;   // host copy (work list, accounting)
 };
 void launch_attn_prefill(const PrefillArgs& a, cudaStream_t st);
 bool attn_prefill_tc(const PrefillArgs& a, int q_rows, cudaStream_t st, double bytes, double flops);

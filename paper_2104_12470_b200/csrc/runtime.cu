@@ -480,7 +480,12 @@ struct StepPlan {
   std::vector<int> h_pads; // host copy: uploads are skipped when unchanged
   int2* rinfo = nullptr;   // [T] (b, t_local)
   int* rowbase = nullptr;  // [b] packed row of slot s = rowbase[b] + s
-  int* pads = nullptr;     // [b]
+  int* pads = nullptr;     // [b] first valid slot
+  // per-sequence valid end (right padding / explicit windows, prompt phase):
+  // empty = every sequence ends at seq
+  std::vector<int> h_ends;
+  int* ends = nullptr;     // [b] device copy, nullptr when h_ends is empty
+  int* ends_buf = nullptr;
 };
 
 struct eet_runtime {
@@ -527,14 +532,20 @@ static void plan_alloc(eet_runtime* rt, StepPlan& p) {
   p.rinfo = (int2*)rt->dev(sizeof(int2) * (size_t)rt->bmax * rt->smax);
   p.rowbase = (int*)rt->dev(sizeof(int) * rt->bmax);
   p.pads = (int*)rt->dev(sizeof(int) * rt->bmax);
+  p.ends_buf = (int*)rt->dev(sizeof(int) * rt->bmax);
 }
 
 // Host-side packing of the valid tokens (pad skipping): prompt rows are the
 // slots [pad_b, t) of each sequence, incremental rows are every sequence.
 // The device copies are refreshed only when the batch layout changes.
+// ends (optional, prompt phase): sequence b's valid slots are [pads[b],
+// ends[b]) instead of [pads[b], seq) — right-padded / windowed batches
+// (the reference itself is left-pad only)
 static void plan_fill(StepPlan& p, int batch, int t, const int* pads, int seq, int phase,
-                      cudaStream_t st) {
-  if (p.valid && p.batch == batch && p.t == t && p.seq == seq && p.phase == phase &&
+                      cudaStream_t st, const int* ends = nullptr) {
+  const bool same_ends = ends ? (p.h_ends.size() == (size_t)batch && std::equal(ends, ends + batch, p.h_ends.begin()))
+                              : p.h_ends.empty();
+  if (p.valid && p.batch == batch && p.t == t && p.seq == seq && p.phase == phase && same_ends &&
       std::equal(pads, pads + batch, p.h_pads.begin()))
     return;
   std::vector<int2> ri;
@@ -542,8 +553,9 @@ static void plan_fill(StepPlan& p, int batch, int t, const int* pads, int seq, i
   ri.reserve((size_t)batch * t);
   for (int b = 0; b < batch; ++b) {
     int first = (phase == EET_PHASE_PROMPT) ? pads[b] : 0;
+    const int last = (ends && phase == EET_PHASE_PROMPT) ? ends[b] : t;
     rb[b] = (int)ri.size() - first;
-    for (int s = first; s < t; ++s) ri.push_back(make_int2(b, s));
+    for (int s = first; s < last; ++s) ri.push_back(make_int2(b, s));
   }
   p.T = (int)ri.size();
   p.batch = batch;
@@ -557,6 +569,14 @@ static void plan_fill(StepPlan& p, int batch, int t, const int* pads, int seq, i
                                    cudaMemcpyHostToDevice, st));
   EET_CHECK_CUDA(cudaMemcpyAsync(p.rowbase, rb.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, st));
   EET_CHECK_CUDA(cudaMemcpyAsync(p.pads, pads, sizeof(int) * batch, cudaMemcpyHostToDevice, st));
+  if (ends) {
+    p.h_ends.assign(ends, ends + batch);
+    EET_CHECK_CUDA(cudaMemcpyAsync(p.ends_buf, ends, sizeof(int) * batch, cudaMemcpyHostToDevice, st));
+    p.ends = p.ends_buf;
+  } else {
+    p.h_ends.clear();
+    p.ends = nullptr;
+  }
   p.valid = true;
 }
 
@@ -635,6 +655,8 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     a.o = ctx.ptr; a.ldo = hq; a.o_rowbase = p.rowbase;
     a.pads = p.pads;
     a.h_pads = p.h_pads.data();
+    a.ends = p.ends;
+    a.h_ends = p.h_ends.empty() ? nullptr : p.h_ends.data();
     a.batch = p.batch; a.seq = p.seq; a.heads = rt->heads; a.hd = rt->hd;
     a.scale = scale;
     a.causal = causal ? 1 : 0;
@@ -819,6 +841,39 @@ int eet_decoder_layer_forward(eet_runtime* rt, float* x, long long x_sb, long lo
   StepPlan& p = rt->plans[0];
   plan_fill(p, batch, t, h_pads, seq_len, phase, S(stream));
   layer_impl(rt, p, x, x_sb, x_ss, w, kc, vc, nullptr, kv_filled, true, kv_filled + t, S(stream));
+  EET_API_END
+}
+
+static void check_windows(const eet_runtime* rt, int batch, int t, const int* h_start, const int* h_end) {
+  EET_REQUIRE(batch >= 1 && batch <= rt->bmax && t >= 1 && t <= rt->smax, EET_ERR_SHAPE,
+              "batch / length exceed runtime capacity");
+  for (int b = 0; b < batch; ++b)
+    EET_REQUIRE(h_start[b] >= 0 && h_start[b] < h_end[b] && h_end[b] <= t, EET_ERR_SHAPE,
+                "window outside [0, seq_len) or empty");
+}
+
+int eet_decoder_layer_forward_window(eet_runtime* rt, float* x, long long x_sb, long long x_ss, int batch,
+                                     int t, const eet_layer_weights* w, void* kc, void* vc, const int* h_start,
+                                     const int* h_end, void* stream) {
+  EET_API_BEGIN
+  check_windows(rt, batch, t, h_start, h_end);
+  StepPlan& p = rt->plans[0];
+  plan_fill(p, batch, t, h_start, t, EET_PHASE_PROMPT, S(stream), h_end);
+  layer_impl(rt, p, x, x_sb, x_ss, w, kc, vc, nullptr, 0, true, t, S(stream));
+  EET_API_END
+}
+
+int eet_encoder_layer_forward_window(eet_runtime* rt, float* x, long long x_sb, long long x_ss, int batch,
+                                     int t, const eet_layer_weights* w, const int* h_start, const int* h_end,
+                                     void* stream) {
+  EET_API_BEGIN
+  check_windows(rt, batch, t, h_start, h_end);
+  StepPlan& p = rt->plans[0];
+  plan_fill(p, batch, t, h_start, t, EET_PHASE_PROMPT, S(stream), h_end);
+  const size_t kvb = (size_t)batch * rt->heads * rt->smax * rt->hd * dtype_size(rt->dtype);
+  Claim kbuf(rt->pool, kvb, EET_SCOPE_WITHIN, "attention.key");
+  Claim vbuf(rt->pool, kvb, EET_SCOPE_WITHIN, "attention.value");
+  layer_impl(rt, p, x, x_sb, x_ss, w, kbuf.ptr, vbuf.ptr, nullptr, 0, false, t, S(stream));
   EET_API_END
 }
 

@@ -130,14 +130,23 @@ def decoder_layer_forward(x, w: LayerWeights, kv: KVCache, desc: BatchDescriptor
     cfg = kv.config
     if h != cfg.hidden_size:
         raise ValueError(f"hidden {h} does not match the cache's {cfg.hidden_size}")
+    right = getattr(desc, "padding_side", "left") == "right"
+    if right and phase is Phase.INCREMENTAL:
+        raise ValueError("incremental step needs a left-padded batch (one common cache cursor)")
     dl = DeviceLayer.of(w, kv.dtype)
     rt = pool.runtime(kv.dtype, h, kv.head_count, cfg.batch_size, cfg.max_sequence)
     xd, wb = _hidden_on_device(x)
     ph = _lib.PHASE_INCREMENTAL if phase is Phase.INCREMENTAL else _lib.PHASE_PROMPT
     try:
-        _lib.call("eet_decoder_layer_forward", rt, xd.data_ptr(), xd.stride(0), xd.stride(1), b, t,
-                  C.byref(dl.c), kv._k[layer_idx].data_ptr(), kv._v[layer_idx].data_ptr(), kv.filled,
-                  _pads_c(desc), desc.seq_len, ph, _stream())
+        if right:                                        # native windows [0, len_b)
+            starts, ends = zip(*desc.windows())
+            _lib.call("eet_decoder_layer_forward_window", rt, xd.data_ptr(), xd.stride(0), xd.stride(1), b, t,
+                      C.byref(dl.c), kv._k[layer_idx].data_ptr(), kv._v[layer_idx].data_ptr(),
+                      (C.c_int * b)(*starts), (C.c_int * b)(*ends), _stream())
+        else:
+            _lib.call("eet_decoder_layer_forward", rt, xd.data_ptr(), xd.stride(0), xd.stride(1), b, t,
+                      C.byref(dl.c), kv._k[layer_idx].data_ptr(), kv._v[layer_idx].data_ptr(), kv.filled,
+                      _pads_c(desc), desc.seq_len, ph, _stream())
     finally:
         pool._sync_log()
     if wb:
@@ -163,8 +172,13 @@ def encoder_layer_forward(x, w: LayerWeights, desc: BatchDescriptor, pool: Buffe
     rt = pool.runtime(dt, h, head_count, b, t)
     xd, wb = _hidden_on_device(x)
     try:
-        _lib.call("eet_encoder_layer_forward", rt, xd.data_ptr(), xd.stride(0), xd.stride(1), b, t,
-                  C.byref(dl.c), _pads_c(desc), _stream())
+        if getattr(desc, "padding_side", "left") == "right":
+            starts, ends = zip(*desc.windows())
+            _lib.call("eet_encoder_layer_forward_window", rt, xd.data_ptr(), xd.stride(0), xd.stride(1), b, t,
+                      C.byref(dl.c), (C.c_int * b)(*starts), (C.c_int * b)(*ends), _stream())
+        else:
+            _lib.call("eet_encoder_layer_forward", rt, xd.data_ptr(), xd.stride(0), xd.stride(1), b, t,
+                      C.byref(dl.c), _pads_c(desc), _stream())
     finally:
         pool._sync_log()
     if wb:

@@ -256,3 +256,17 @@ def test_device_cache_fingerprint_tracks_source_arrays():
     fpt = _fingerprint([t])
     t.add_(1.0)                                      # in-place: torch version counter
     assert _fingerprint([t]) != fpt
+
+
+def test_right_padded_batch_descriptor():
+    """make_batch(padding_side='right'): pads at the end, valid windows
+    [0, len_b); the reference's left padding stays the default."""
+    import paper_2104_12470_b200 as eet
+    d = eet.make_batch([5, 2, 4, 10], padding_side="right")
+    assert d.padding_len == (5, 8, 6, 0) and d.padding_side == "right"
+    assert d.windows() == [(0, 5), (0, 2), (0, 4), (0, 10)]
+    left = eet.make_batch([5, 2, 4, 10])
+    assert left.padding_side == "left" and left.windows() == [(5, 10), (8, 10), (6, 10), (0, 10)]
+    import pytest
+    with pytest.raises(ValueError):
+        eet.BatchDescriptor(seq_len=4, padding_len=(1,), batch=1, padding_side="middle")
