@@ -358,3 +358,47 @@ def test_tensor_parallel_shards_sum_to_full_layer(eet, dt, h, heads, tp, lengths
     for i, pad in enumerate(desc.padding_len):
         combined_close(got[i, pad:], ref[i, pad:], tol, f"tp{tp} prompt row {i}")
     combined_close(x1.cpu().numpy(), ref1, tol, f"tp{tp} decode step")
+
+
+
+def test_ffn_chunked_reference_memory_shape(cuda_ok):
+    """EET_FFN_CHUNKED=1 (fp32): the FFN intermediate is accumulated in two
+    half-width chunks like the reference (runtime.py:195-214): no pool
+    request wider than T x 2h, oracle parity at 1e-5, and the same greedy
+    tokens as the default whole-width path (this process)."""
+    import os
+    import subprocess
+    import sys
+    import paper_2104_12470_b200 as eet
+    code = r'''
+import numpy as np, paper_2104_12470_b200 as eet
+from oracle import eet_oracle as orc
+cfg = eet.ModelConfig(batch_size=2, hidden_size=256, layer_count=2, head_count=4, max_prompt=40, max_sequence=48)
+w = eet.random_weights(cfg, vocab=64, seed=4)
+desc = eet.make_batch([40, 23])
+x = np.random.default_rng(1).normal(0, 1, size=(2, 40, 256)).astype(np.float32)
+kv, acts = eet.preallocate_caches(cfg)
+log = eet.AllocationLog()
+out = eet.decoder_layer_forward(x.copy(), w.layers[0], kv, desc, eet.Phase.PROMPT_PARALLEL,
+                                eet.BufferPool(log=log), acts, 0)
+okv = orc.OracleKV(2, 4, 40, 64, 1)
+ref = orc.decoder_layer(x, w.layers[0], okv, desc.padding_len, 0, 4)
+for i, p in enumerate(desc.padding_len):
+    err = np.abs(out[i, p:] - ref[i, p:]).max() / (1 + np.abs(ref[i, p:]).max())
+    assert err < 1e-5, err
+T = sum(40 - p for p in desc.padding_len)
+mids = [r.size for r in log.records if r.event == "request" and r.tag == "ffn.intermediate"]
+assert mids and max(mids) <= T * 2 * 256, mids
+req = eet.GenerationRequest(prompts=[[1, 2, 3, 4, 5], [7, 8]], steps=6)
+print("TOKENS", eet.generate(w, req, cfg).tolist())
+'''
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, EET_FFN_CHUNKED="1", PYTHONPATH=repo)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    toks = [l for l in r.stdout.splitlines() if l.startswith("TOKENS")][0]
+    cfg = eet.ModelConfig(batch_size=2, hidden_size=256, layer_count=2, head_count=4, max_prompt=40,
+                          max_sequence=48)
+    w = eet.random_weights(cfg, vocab=64, seed=4)
+    req = eet.GenerationRequest(prompts=[[1, 2, 3, 4, 5], [7, 8]], steps=6)
+    assert toks == "TOKENS " + str(eet.generate(w, req, cfg).tolist())
