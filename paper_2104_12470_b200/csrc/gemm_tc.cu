@@ -157,6 +157,7 @@ __device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int 
 
 struct L2Plan {
   int gm;                  // M-tiles per raster group
+  int resid_pipe;          // pipelined residual epilogue (A/B: EET_GEMM_RESID_PIPE=0)
   uint64_t pol_a, pol_b;   // L2 cache policies of the A / B TMA loads
 };
 
@@ -261,9 +262,59 @@ __global__ void __launch_bounds__(THREADS, 1)
       tile_coords(tile, num_m, num_n, L.gm, mb, nb);
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
+      const int m = mb * BM + row;
+      // Residual epilogue (out-proj / W2): the fp32 row segment x[m, nb*BN ..
+      // +BN) is read-modify-written. Its loads are issued two 32-column
+      // chunks ahead (the first two before the accumulator is ready), so
+      // the row's DRAM latency is paid ~once per tile instead of once per
+      // 8 columns (c4 out-proj, K = 4096: the per-chunk load stalls made
+      // the epilogue longer than the tile's MMA).
+      float* xrow = nullptr;
+      if (e.mode == EPI_RESID && m < M && nb * BN + BN <= N) {
+        const int2 rr = e.rinfo[m];
+        xrow = e.x + rr.x * e.x_sb + rr.y * e.x_ss + nb * BN;
+        if ((reinterpret_cast<uintptr_t>(xrow) | reinterpret_cast<uintptr_t>(e.bias)) & 15) xrow = nullptr;
+      }
+      // tcgen05.ld is warp-collective: the whole warp takes one path
+      if (__all_sync(0xffffffffu, xrow != nullptr) && L.resid_pipe) {
+        constexpr int NCH = BN / 32;
+        float4 xv[NCH][8];
+#pragma unroll
+        for (int c = 0; c < 2 && c < NCH; ++c)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xv[c][j] = *reinterpret_cast<const float4*>(xrow + c * 32 + j * 4);
+        mbar_wait(&tfull[as], aphase);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          if (c + 2 < NCH) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xv[c + 2][j] = *reinterpret_cast<const float4*>(xrow + (c + 2) * 32 + j * 4);
+          }
+          uint32_t r[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c * 32, r);
+          const int n0 = nb * BN + c * 32;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 a = xv[c][j];
+            float b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
+            if (e.bias) {
+              const float4 bb = *reinterpret_cast<const float4*>(e.bias + n0 + j * 4);
+              b0 = bb.x; b1 = bb.y; b2 = bb.z; b3 = bb.w;
+            }
+            a.x += __uint_as_float(r[j * 4 + 0]) + b0;
+            a.y += __uint_as_float(r[j * 4 + 1]) + b1;
+            a.z += __uint_as_float(r[j * 4 + 2]) + b2;
+            a.w += __uint_as_float(r[j * 4 + 3]) + b3;
+            *reinterpret_cast<float4*>(xrow + c * 32 + j * 4) = a;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[as]);
+        continue;
+      }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const int m = mb * BM + row;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
@@ -337,6 +388,11 @@ static void launch(const void* A, int lda, const void* B, int ldb, int M, int N,
   if (num_m <= 32 && (long long)num_m * panel_row_bytes <= (96LL << 20)) L.gm = num_m;
   L.pol_a = EVICT_LAST;
   L.pol_b = EVICT_NORMAL;
+  static const int resid_pipe = [] {
+    const char* v = std::getenv("EET_GEMM_RESID_PIPE");
+    return v ? atoi(v) : 1;
+  }();
+  L.resid_pipe = resid_pipe;
   if (mode == 0) {                       // previous plan: GM 32, A evict-first, B evict-last
     L.gm = 32;
     L.pol_a = EVICT_FIRST;
