@@ -62,6 +62,7 @@ WORKLOADS = {
                lengths="full", tp_ok=True, desc="decoder layer h12288 96 heads s2048 b1, bf16"),
 }
 
+E2E_DEPTH = 3          # layer workloads: steps in flight in the e2e measurement (copy/compute overlap)
 HBM_KINDS = {"attn_decode", "gemv", "layernorm", "embed", "argmax", "softmax", "advance", "decode_step"}
 
 
@@ -452,10 +453,11 @@ def main():
     kind = w.get("kind", "generate")
     hbm, tflops, peak_src = peaks()
     if w["dtype"] == "fp32":
-        # fp32 mode runs true-FP32 FFMA on the CUDA cores (no TF32, SURVEY
-        # App. B.4): its roofline is the FP32 SIMT peak, not in
-        # MEASURED_PEAKS.json, so measured here: cuBLAS fp32 GEMM with TF32
-        # off (SURVEY §8(d) protocol), best of 5 at 8192^3
+        # fp32 mode computes at fp32 accuracy (3xTF32 on the tensor cores,
+        # FFMA for decode rows; no plain TF32): its roofline
+        # is the FP32 peak, not in MEASURED_PEAKS.json, so measured here:
+        # cuBLAS fp32 GEMM with TF32 off (SURVEY §8(d) protocol), best of 5
+        # at 8192^3
         tflops, peak_src = measure_fp32_peak(torch), "measured: torch.matmul fp32, allow_tf32=False, 8192^3"
     if kind == "generate":
         cfg = eet.ModelConfig(batch_size=w["batch"], hidden_size=w["hidden"], layer_count=w["layers"],
@@ -529,14 +531,47 @@ def main():
         x_pin = torch.from_numpy(x_host).pin_memory()
         out_pin = torch.empty_like(x_pin).pin_memory()
         units = sum(lens)
-        h2d = d2h = x_host.nbytes
+        # heavily padded batches (c3: 44% valid) copy only each sequence's
+        # valid slots [start, end); otherwise one copy of the whole array
+        windows = desc.windows() if units * w["hidden"] * 4 < 0.7 * x_host.nbytes else None
+        h2d = d2h = units * w["hidden"] * 4 if windows else x_host.nbytes
+
+        # e2e: every step copies its valid hidden-state rows pinned host -> device, runs
+        # the layer through the public API and copies the result back to
+        # pinned host memory. E2E_DEPTH independent contexts (stream, K/V
+        # cache, buffer pool, device buffer) take the steps in turn, so one
+        # step's host->device copy, another's layer and a third's
+        # device->host copy overlap (the two copy engines and the SMs are
+        # separate resources) -- how a server keeps the GPU busy between
+        # requests.
+        ctxs = []
+        for i in range(E2E_DEPTH):
+            kv_i, acts_i = (kv, acts) if i == 0 else eet.preallocate_caches(cfg)
+            ctxs.append({"s": torch.cuda.Stream(), "kv": kv_i, "acts": acts_i,
+                         "pool": pool if i == 0 else eet.BufferPool(), "x": torch.empty_like(x_dev),
+                         "out": torch.empty_like(x_pin).pin_memory()})
+        host_i = [0]
 
         def step(graph=True, host=False):
+            if host:
+                c = ctxs[host_i[0] % len(ctxs)]
+                host_i[0] += 1
+                with torch.cuda.stream(c["s"]):
+                    c["kv"]._filled = 0
+                    if windows is None:
+                        c["x"].copy_(x_pin, non_blocking=True)
+                    else:                                          # valid rows only: pad rows are
+                        for i, (a0, a1) in enumerate(windows):     # never read ...
+                            c["x"][i, a0:a1].copy_(x_pin[i, a0:a1], non_blocking=True)
+                    eet.decoder_layer_forward(c["x"], lw, c["kv"], desc, eet.Phase.PROMPT_PARALLEL, c["pool"],
+                                              c["acts"], 0)
+                    if windows is None:
+                        c["out"].copy_(c["x"], non_blocking=True)
+                    else:                                          # ... nor written by the layer
+                        for i, (a0, a1) in enumerate(windows):
+                            c["out"][i, a0:a1].copy_(c["x"][i, a0:a1], non_blocking=True)
+                return c["out"]
             kv._filled = 0
-            if host:                               # e2e: pinned host -> device -> pinned host
-                xd = x_pin.to("cuda", non_blocking=True)
-                eet.decoder_layer_forward(xd, lw, kv, desc, eet.Phase.PROMPT_PARALLEL, pool, acts, 0)
-                return out_pin.copy_(xd, non_blocking=True)
             return eet.decoder_layer_forward(x_dev, lw, kv, desc, eet.Phase.PROMPT_PARALLEL, pool, acts, 0)
 
     clk = ClockSampler(torch.cuda.current_device()).__enter__()   # running before the warm-up
@@ -574,6 +609,10 @@ def main():
     value = units_all * args.steps / (ms / 1e3)
 
     # end to end through the public API: host inputs in, host results out
+    if kind != "generate" and not tp_mode:
+        for _ in range(E2E_DEPTH):                 # first use of every context outside the timing
+            step(host=True)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step(host=True) if kind != "generate" else step()

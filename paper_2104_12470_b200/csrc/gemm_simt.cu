@@ -10,7 +10,9 @@
 #include "sm100.cuh"
 
 #include <algorithm>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 namespace eet {
 
@@ -151,22 +153,28 @@ void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M, int 
   if (M <= 0 || N <= 0) return;
   const int tiles = ((N + BN - 1) / BN) * ((M + BM - 1) / BM);
   int splits = std::max(1, std::min(2 * device_sm_count() / std::max(1, tiles), K / 128));
-  static float* ws = nullptr;
-  static size_t ws_bytes = 0;
+  float* ws = nullptr;
   if (splits > 1) {
+    // per-stream split-K workspace (concurrent layers on several streams),
+    // grown outside graph capture (unsplit under capture if too small)
+    static std::mutex mu;
+    static std::unordered_map<cudaStream_t, std::pair<float*, size_t>> wss;
     const size_t need = sizeof(float) * (size_t)splits * M * N;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    if (need > ws_bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto& slot = wss[st];
+    if (need > slot.second) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
       if (cs != cudaStreamCaptureStatusNone) {
         splits = 1;
       } else {
         EET_CHECK_CUDA(cudaStreamSynchronize(st));
-        if (ws) cudaFree(ws);
-        EET_CHECK_CUDA(cudaMalloc(&ws, need));
-        ws_bytes = need;
+        if (slot.first) cudaFree(slot.first);
+        EET_CHECK_CUDA(cudaMalloc(&slot.first, need));
+        slot.second = need;
       }
     }
+    if (splits > 1) ws = slot.first;
   }
   const int kspan = ((K + splits - 1) / splits + BK - 1) / BK * BK;
   splits = (K + kspan - 1) / kspan;
@@ -175,9 +183,9 @@ void gemm_f32_simt(const float* A, int lda, const float* B, int ldb, int M, int 
   const bool vec = lda % 4 == 0 && ldb % 4 == 0 && kspan % 4 == 0 &&
                    (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
   if (vec)
-    gemm_f32_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, splits > 1 ? ws : nullptr);
+    gemm_f32_kernel<true><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, ws);
   else
-    gemm_f32_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, splits > 1 ? ws : nullptr);
+    gemm_f32_kernel<false><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, e, kspan, ws);
   EET_LAUNCH_CHECK();
   if (splits > 1) {
     const long long total = (long long)M * N;
