@@ -354,14 +354,23 @@ def ablation_roofline(step, args, ms_full, w, hbm, torch, _lib):
     {class: (delta ms per generate, algorithmic bytes per generate, launches)}."""
     h, L, V, es, b = w["hidden"], w["layers"], w["vocab"], 2, w["batch"]
     steps, p = w["steps"], w["prompt"]
-    classes = {
-        # decode projections (gemv_cl): every weight of every layer once per step
-        "gemv_cl": ("qkv,o,w1,w2", steps * L * 12 * h * h * es, steps * L * 4),
-        # decode attention: every cached K/V row of the batch once per step
-        "attn_decode": ("attn", sum(b * 2 * h * es * L * (p + s + 1) for s in range(steps)), steps * L),
-        # LM head + fused argmax
-        "lm_head": ("head", steps * V * h * es, steps),
-    }
+    kv = sum(b * 2 * h * es * L * (p + s + 1) for s in range(steps))
+    if os.environ.get("EET_ATTN_O", "1") != "0":
+        classes = {
+            # decode projections (gemv_cl): QKV (+LN1), W1 (+LN2, GELU), W2 (+residual)
+            "gemv_cl": ("qkv,w1,w2", steps * L * 11 * h * h * es, steps * L * 3),
+            # decode attention fused with the out-projection (attn_o.cu): every
+            # cached K/V row of the batch + W_o once per step
+            "attn_o": ("attn,o", kv + steps * L * h * h * es, steps * L),
+            # LM head + fused argmax
+            "lm_head": ("head", steps * V * h * es, steps),
+        }
+    else:
+        classes = {
+            "gemv_cl": ("qkv,o,w1,w2", steps * L * 12 * h * h * es, steps * L * 4),
+            "attn_decode": ("attn", kv, steps * L),
+            "lm_head": ("head", steps * V * h * es, steps),
+        }
     out = {}
     reps = max(2, min(args.steps, 3))
     for name, (spec, byts, launches) in classes.items():

@@ -92,8 +92,18 @@ enum EpiMode : int {
   EPI_ARGMAX = 5,     // LM head: greedy token per row (lm_head_argmax only), optional logits
 };
 
+// Pending residual in 2^-32 fixed point (decode out-projection, attn_o.cu):
+// contributions are added with integer atomics, so their sum does not
+// depend on arrival order; consumers read x + pend(acc) and the W2 epilogue
+// folds it into x and re-zeroes it.
+constexpr float kAccScale = 4294967296.0f;            // 2^32
+constexpr float kAccInv = 2.3283064365386963e-10f;    // 2^-32
+__device__ __forceinline__ float acc_to_f(long long a) { return __ll2float_rn(a) * kAccInv; }
+
 struct Epi {
   int mode = EPI_STORE_F32;
+  long long* acc = nullptr;       // EPI_RESID (decode GEMV): pending fixed-point residual rows, ld acc_sb
+  long long acc_sb = 0;
   const float* bias = nullptr;
   void* out = nullptr;
   int ldo = 0;
@@ -203,11 +213,19 @@ struct DecodeArgs {
   unsigned long long kv_policy = 0;    // L2 cache hint of the K/V bulk copies (0: none)
 };
 void launch_attn_decode(const DecodeArgs& a, cudaStream_t st);
+// decode attention fused with the out-projection + residual (attn_o.cu);
+// false when not eligible (16-bit, hd 64/128, one CTA per (sequence, head))
+bool launch_attn_o(const DecodeArgs& a, const void* wo, int h, long long* acc, long long acc_sb,
+                   const float* bias, cudaStream_t st);
 
 // ---- decode projections / LM head straight from the K-major weights (gemv_cl.cu)
+// acc (LayerNorm source only): pending fixed-point residual rows added to x
 bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
              long long x_sb, long long x_ss, const int2* rinfo, const float* g, const float* b, const Epi& e,
-             cudaStream_t st);
+             cudaStream_t st, const long long* acc = nullptr, long long acc_sb = 0);
+// would gemv_cl take this projection (same checks, no launch)
+bool gemv_cl_ok(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
+                long long x_sb, const float* g, const float* b, int mode);
 bool lm_head_argmax(int dtype, const void* W, int M, int N, int K, const float* x, long long x_sb, long long x_ss,
                     const int2* rinfo, const float* g, const float* b, const Epi& e, cudaStream_t st);
 // decode attention split plan (attention.cu)

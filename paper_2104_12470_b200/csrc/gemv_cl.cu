@@ -32,7 +32,7 @@
 // of the token rows is staged once per CTA, then 16-row vocab tiles stream
 // through a 4-stage TMA ring; each CTA keeps a running (max, lowest id) per
 // token and argmax_cand_kernel reduces the per-CTA candidates.
-#include "sm100.cuh"
+#include "mma_frag.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -67,6 +67,8 @@ struct LnSrc {                              // fused-LayerNorm operand source
   long long x_sb;
   const float* g;
   const float* b;
+  const long long* acc;                     // pending fixed-point residual rows (or null), ld acc_sb
+  long long acc_sb;
 };
 
 struct Shape {
@@ -97,97 +99,6 @@ struct Lay {
   }
 };
 
-__device__ __forceinline__ void ldmatrix_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                            uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-
-// remote (DSMEM) stores that complete_tx on the receiver's mbarrier
-__device__ __forceinline__ void st_async_v4(uint32_t addr, const float* v, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
-               ::"r"(addr), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "r"(mbar)
-               : "memory");
-}
-__device__ __forceinline__ void st_async_v2(uint32_t addr, float a, float b, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
-               ::"r"(addr), "f"(a), "f"(b), "r"(mbar)
-               : "memory");
-}
-
-template <typename T>
-__device__ __forceinline__ void mma16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-        "{%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-  } else {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-        "{%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-  }
-}
-
-// A fragment of the 16x16 weight sub-tile (rows row0.., k-step ks) from a
-// weight block laid out as [Kc/64 boxes][rows][64] with 128B swizzle
-__device__ __forceinline__ void load_a(uint32_t sw, int rows, int row0, int ks, int lane, uint32_t* a) {
-  const int r = row0 + (lane & 15);
-  const int chunk = ((ks & 3) << 1) | (lane >> 4);              // 16-byte chunk within the 128 B row
-  const uint32_t addr = sw + (uint32_t)((ks >> 2) * rows * 128 + r * 128 + ((chunk ^ (r & 7)) << 4));
-  ldmatrix_x4(addr, a[0], a[1], a[2], a[3]);
-}
-
-// one warp: tile rows [row0, row0+16) x k-steps [s0, s1) x NB n-blocks of
-// token rows; four independent accumulator chains, summed in a fixed order
-template <typename T, int NB>
-__device__ __forceinline__ void warp_mma(uint32_t sw, int rows, int row0, int s0, int s1, const T* xs,
-                                         int xst, int lane, float (&acc)[NB][4]) {
-  float part[4][NB][4];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) part[c][nb][i] = 0.f;
-  const int g = lane >> 2, c4 = lane & 3;
-  int s = s0;
-#pragma unroll 1
-  for (; s + 3 < s1; s += 4) {
-    uint32_t a[4][4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) load_a(sw, rows, row0, s + c, lane, a[c]);
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb) {
-        const T* xr = xs + (nb * 8 + g) * xst + (s + c) * 16 + 2 * c4;
-        mma16816<T>(part[c][nb], a[c][0], a[c][1], a[c][2], a[c][3], *reinterpret_cast<const uint32_t*>(xr),
-                    *reinterpret_cast<const uint32_t*>(xr + 8));
-      }
-  }
-#pragma unroll 1
-  for (; s < s1; ++s) {
-    uint32_t a[4];
-    load_a(sw, rows, row0, s, lane, a);
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-      const T* xr = xs + (nb * 8 + g) * xst + s * 16 + 2 * c4;
-      mma16816<T>(part[0][nb], a[0], a[1], a[2], a[3], *reinterpret_cast<const uint32_t*>(xr),
-                  *reinterpret_cast<const uint32_t*>(xr + 8));
-    }
-  }
-#pragma unroll
-  for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[nb][i] = (part[0][nb][i] + part[1][nb][i]) + (part[2][nb][i] + part[3][nb][i]);
-}
-
 // decode epilogue (one mode per kernel instance: compact code): token row
 // m is sequence m at cache slot kvs (runtime.py:136 cache write, :188/:212
 // residual, :206-209 GELU)
@@ -201,7 +112,14 @@ __device__ __forceinline__ void dec_epi(const Epi& e, int kvs, int m, int n, flo
   } else if constexpr (MODE == EPI_GELU_T) {
     reinterpret_cast<T*>(e.out)[(long long)m * e.ldo + n] = from_f<T>(gelu_tanh(v));
   } else if constexpr (MODE == EPI_RESID) {
-    e.x[m * e.x_sb + n] += v;
+    float* xp = e.x + m * e.x_sb + n;
+    if (e.acc) {                                    // fold in the pending out-projection, re-zero it
+      long long* ap = e.acc + m * e.acc_sb + n;
+      *xp = (*xp + acc_to_f(*ap)) + v;
+      *ap = 0;
+    } else {
+      *xp += v;
+    }
   } else if constexpr (MODE == EPI_QKV) {
     if (n < e.hq) {
       reinterpret_cast<T*>(e.out)[(long long)m * e.hq + n] = from_f<T>(v);
@@ -307,9 +225,26 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
       const bool live = lrow < sh.M;
       const float4* xr = reinterpret_cast<const float4*>(
           dry ? ln.g + k0 : ln.x + (live ? lrow : 0) * ln.x_sb + k0);
+      // x + the pending out-projection (attn_o.cu), both loads in flight together
+      const bool pend = ln.acc && live && !dry;
+      const longlong2* ar = reinterpret_cast<const longlong2*>(ln.acc + (pend ? lrow * ln.acc_sb + k0 : 0));
+      longlong2 pa[LNV][2];
 #pragma unroll
-      for (int j = 0; j < LNV; ++j)
+      for (int j = 0; j < LNV; ++j) {
         v[j] = (live && j < nv) ? xr[j * 16 + lsub] : make_float4(0.f, 0.f, 0.f, 0.f);
+        pa[j][0] = pa[j][1] = make_longlong2(0, 0);
+        if (pend && j < nv) {
+          pa[j][0] = ar[(j * 16 + lsub) * 2];
+          pa[j][1] = ar[(j * 16 + lsub) * 2 + 1];
+        }
+      }
+      if (pend) {
+#pragma unroll
+        for (int j = 0; j < LNV; ++j) {
+          v[j].x += acc_to_f(pa[j][0].x); v[j].y += acc_to_f(pa[j][0].y);
+          v[j].z += acc_to_f(pa[j][1].x); v[j].w += acc_to_f(pa[j][1].y);
+        }
+      }
       // slice mean and M2 (two passes over registers), 16 lanes per row
       float s = 0.f;
 #pragma unroll
@@ -744,23 +679,37 @@ static void go(const CUtensorMap& mw, const LnSrc& ln, const Shape& sh, size_t s
 // b). Decode rows only: token m is sequence m at slot 0, i.e. x row m at
 // x + m * x_sb (rinfo[m] == (m, 0) in the incremental plan) and the epilogue
 // row is m. False when the shape is not eligible (caller falls back).
-bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
-             long long x_sb, long long x_ss, const int2* rinfo, const float* g, const float* b, const Epi& e,
-             cudaStream_t st) {
+static bool cl_check(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
+                     long long x_sb, const float* g, const float* b, int mode, gc::Shape& sh, size_t& smem) {
   if (dtype != EET_F16 && dtype != EET_BF16) return false;
   const bool ln = x != nullptr;
-  if (ln ? (e.mode != EPI_QKV && e.mode != EPI_GELU_T && e.mode != EPI_STORE_F32)
-         : (e.mode != EPI_RESID && e.mode != EPI_STORE_F32 && e.mode != EPI_STORE_T && e.mode != EPI_GELU_T))
+  if (ln ? (mode != EPI_QKV && mode != EPI_GELU_T && mode != EPI_STORE_F32)
+         : (mode != EPI_RESID && mode != EPI_STORE_F32 && mode != EPI_STORE_T && mode != EPI_GELU_T))
     return false;
   if (ln && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(b)) & 15 ||
-             (x_sb & 3) || (x_ss & 3)))
+             (x_sb & 3)))
     return false;
   if (!ln && ((reinterpret_cast<uintptr_t>(X) & 15) || (ldx % 8))) return false;
   if (reinterpret_cast<uintptr_t>(W) & 15) return false;
+  return gc::plan(M, N, K, M <= 8 ? 1 : 2, sh, smem) && smem <= 227 * 1024;
+}
+
+bool gemv_cl_ok(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
+                long long x_sb, const float* g, const float* b, int mode) {
+  gc::Shape sh{};
+  size_t smem = 0;
+  return cl_check(dtype, W, M, N, K, X, ldx, x, x_sb, g, b, mode, sh, smem);
+}
+
+bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
+             long long x_sb, long long x_ss, const int2* rinfo, const float* g, const float* b, const Epi& e,
+             cudaStream_t st, const long long* acc, long long acc_sb) {
+  const bool ln = x != nullptr;
+  if (ln && (x_ss & 3)) return false;
   const int NB = M <= 8 ? 1 : 2;
   gc::Shape sh{};
   size_t smem = 0;
-  if (!gc::plan(M, N, K, NB, sh, smem) || smem > 227 * 1024) return false;
+  if (!cl_check(dtype, W, M, N, K, X, ldx, x, x_sb, g, b, e.mode, sh, smem)) return false;
   sh.ln = ln ? 1 : 0;
   sh.X = X;
   sh.ldx = ldx;
@@ -775,7 +724,7 @@ bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int l
   }();
   sh.early = early == 1 || (early == 2 && e.mode == EPI_QKV);   // 2: only QKV (its attention streams K/V early)
   (void)x_ss; (void)rinfo;
-  const gc::LnSrc src{x, x_sb, g, b};
+  const gc::LnSrc src{x, x_sb, g, b, acc, acc_sb};
   const CUtensorMap mw = make_tma_map_kblk(W, N, K, K, 16 * sh.NT, sh.Kc / 64, dtype);
   ProfScope ps(K_GEMV, st, (double)N * K * 2 + (double)M * K * (ln ? 4 : 2) + gemm_bytes(M, N, 0, 2, e),
                2.0 * M * N * K);
@@ -803,7 +752,7 @@ bool lm_head_argmax(int dtype, const void* W, int M, int N, int K, const float* 
                       (size_t)gc::HCW * 16 * 8 + gc::HSTAGES * 16 + 1024 + 64;
   const CUtensorMap mw = make_tma_map_kblk(W, N, K, K, 16, K / 64, dtype);
   (void)x_ss; (void)rinfo;                       // rows: x + m * x_sb (decode plan)
-  const gc::LnSrc src{x, x_sb, g, b};
+  const gc::LnSrc src{x, x_sb, g, b, nullptr, 0};
   {
     ProfScope ps(K_GEMV, st, (double)N * K * 2 + (double)M * K * 4, 2.0 * M * N * K);
     auto run = [&](auto kern) {

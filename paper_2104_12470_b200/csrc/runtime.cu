@@ -506,6 +506,7 @@ struct eet_runtime {
   int* h_prompts = nullptr;           // pinned staging: prompts in, tokens out
   long long* h_tokens = nullptr;
   float* xdec = nullptr;              // decode residual stream [bmax, h]
+  long long* oacc = nullptr;          // pending out-projection [bmax, h], 2^-32 fixed point, zero between layers
   void* tp_ctx = nullptr;             // tensor parallel: attention context kept for the row-chunked out-proj
   void* tp_mid = nullptr;             // tensor parallel: FFN intermediate kept for the row-chunked W2
   int2* cand = nullptr;               // fused LM-head argmax candidates
@@ -600,14 +601,17 @@ static Epi tp_partial_epi(const eet_runtime* rt, void* partial, const float* bia
   return e;
 }
 
-static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb, long long x_ss,
+// Returns true when the out-projection was fused into the decode attention
+// (attn_o.cu): its result is then pending in rt->oacc and the FFN's LN2 + W1
+// and W2 GEMVs consume it.
+static bool attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb, long long x_ss,
                        const eet_layer_weights* w, void* kc, void* vc, const int* kv_dev,
                        int kv_base, bool causal, int L_host, void* partial, cudaStream_t st,
                        bool keep_ctx = false) {
   const int h = rt->h, hq = rt->hq, T = p.T, dt = rt->dtype;
   const size_t es = dtype_size(dt);
   const int scope = (p.phase == EET_PHASE_PROMPT) ? EET_SCOPE_WITHIN : EET_SCOPE_ACROSS;
-  if (T == 0) return;
+  if (T == 0) return false;
 
   Claim q(rt->pool, (size_t)T * hq * es, scope, "attention.query");
   {
@@ -679,10 +683,28 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     a.counters = rt->counters;
     a.o = ctx.ptr; a.ldo = hq;
     a.splits = rt->splits;
-    if (!skip_decode("attn")) launch_attn_decode(a, st);
+    if (!skip_decode("attn")) {
+      // out-projection fused into the attention kernel (attn_o.cu) when the
+      // FFN GEMVs that consume its pending result take this shape
+      const int f = rt->ffn;
+      if (!keep_ctx && !partial && !skip_decode("o") && (x_ss & 3) == 0 &&
+          gemv_cl_ok(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, w->ln2_g, w->ln2_b, EPI_GELU_T) &&
+          gemv_cl_ok(dt, w->w2, T, h, f, nullptr, f, nullptr, 0, nullptr, nullptr, EPI_RESID)) {
+        if (!rt->oacc) {
+          rt->oacc = (long long*)rt->dev(sizeof(long long) * (size_t)rt->bmax * h);
+          EET_CHECK_CUDA(cudaMemsetAsync(rt->oacc, 0, sizeof(long long) * (size_t)rt->bmax * h, st));
+        }
+        if (launch_attn_o(a, w->wo, h, rt->oacc, h, w->b_o, st)) {
+          q.release();
+          ctx.release();
+          return true;
+        }
+      }
+      launch_attn_decode(a, st);
+    }
   }
   q.release();
-  if (keep_ctx) return;
+  if (keep_ctx) return false;
   {
     Epi e;
     e.bias = w->b_o;
@@ -699,13 +721,17 @@ static void attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
       gemm(dt, ctx.ptr, hq, w->wo, hq, T, h, hq, e, st);
   }
   ctx.release();
+  return false;
 }
 
 // Feed-forward half (runtime.py:192-214): LN2 -> W1 GEMM (+GELU) -> W2 GEMM,
 // residual into x or a tensor-parallel partial as above. Both pool requests
 // use across-module scope like the reference (runtime.py:200-207).
+// acc: pending out-projection rows (attn_block returned true): read by the
+// LN2 prologue of W1, folded into x and re-zeroed by the W2 epilogue.
 static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb, long long x_ss,
-                      const eet_layer_weights* w, void* partial, cudaStream_t st, bool keep_mid = false) {
+                      const eet_layer_weights* w, void* partial, cudaStream_t st, bool keep_mid = false,
+                      long long* acc = nullptr) {
   const int h = rt->h, f = rt->ffn, T = p.T, dt = rt->dtype;
   const size_t es = dtype_size(dt);
   if (T == 0) return;
@@ -754,12 +780,15 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
     e.ldo = f;
     const bool inc = p.phase == EET_PHASE_INCREMENTAL;
     if (inc && skip_decode("w1")) {
-    } else if (inc && gemv_cl(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, e, st)) {
-    } else if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T,
-                                             f, h, e, st))) {
-      Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
-      launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln2_g, w->ln2_b, ln2.ptr, dt, h, h, 0, st);
-      gemm(dt, ln2.ptr, h, w->w1, h, T, f, h, e, st);
+    } else if (inc && gemv_cl(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, e, st, acc,
+                              h)) {
+    } else {
+      EET_REQUIRE(!acc, EET_ERR_UNSUPPORTED, "pending out-projection without its W1 GEMV");
+      if (!(T <= 32 && gemv_tc_ln_sm100(dt, x, x_sb, x_ss, p.rinfo, w->ln2_g, w->ln2_b, w->w1, h, T, f, h, e, st))) {
+        Claim ln2(rt->pool, (size_t)T * h * es, EET_SCOPE_ACROSS, "ffn.layernorm");
+        launch_layer_norm(x, x_sb, x_ss, p.rinfo, T, w->ln2_g, w->ln2_b, ln2.ptr, dt, h, h, 0, st);
+        gemm(dt, ln2.ptr, h, w->w1, h, T, f, h, e, st);
+      }
     }
   }
   if (keep_mid) return;
@@ -772,11 +801,15 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
       e.mode = EPI_RESID;
       e.x = x; e.x_sb = x_sb; e.x_ss = x_ss;
       e.rinfo = p.rinfo;
+      e.acc = acc;
+      e.acc_sb = h;
     }
     if (p.phase == EET_PHASE_INCREMENTAL && skip_decode("w2")) {
     } else if (!(p.phase == EET_PHASE_INCREMENTAL &&
-                 gemv_cl(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st)))
+                 gemv_cl(dt, w->w2, T, h, f, mid.ptr, f, nullptr, 0, 0, nullptr, nullptr, nullptr, e, st))) {
+      EET_REQUIRE(!acc, EET_ERR_UNSUPPORTED, "pending out-projection without its W2 GEMV");
       gemm(dt, mid.ptr, f, w->w2, f, T, h, f, e, st);
+    }
   }
   mid.release();
 }
@@ -785,8 +818,8 @@ static void ffn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x_
 static void layer_impl(eet_runtime* rt, const StepPlan& p, float* x, long long x_sb,
                        long long x_ss, const eet_layer_weights* w, void* kc, void* vc,
                        const int* kv_dev, int kv_base, bool causal, int L_host, cudaStream_t st) {
-  attn_block(rt, p, x, x_sb, x_ss, w, kc, vc, kv_dev, kv_base, causal, L_host, nullptr, st);
-  ffn_block(rt, p, x, x_sb, x_ss, w, nullptr, st);
+  const bool pending = attn_block(rt, p, x, x_sb, x_ss, w, kc, vc, kv_dev, kv_base, causal, L_host, nullptr, st);
+  ffn_block(rt, p, x, x_sb, x_ss, w, nullptr, st, false, pending ? rt->oacc : nullptr);
 }
 
 extern "C" {
@@ -1104,6 +1137,8 @@ int eet_generate(eet_runtime* rt, const eet_model* m, const int* h_prompts, cons
   cudaStream_t st = rt->cs;
   EET_CHECK_CUDA(cudaEventRecord(rt->ev_in, caller));
   EET_CHECK_CUDA(cudaStreamWaitEvent(st, rt->ev_in, 0));
+  if (rt->oacc)                       // pending out-projection: zero between layers, reset per call
+    EET_CHECK_CUDA(cudaMemsetAsync(rt->oacc, 0, sizeof(long long) * (size_t)rt->bmax * rt->h, st));
 
   std::vector<int> pads(batch);
   int t = 0;
