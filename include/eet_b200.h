@@ -172,6 +172,11 @@ int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream)
  * wait passed, X staged, weights landed, partials sent, end (globaltimer),
  * then clock64 offsets of the phase ends of CTA 0]. */
 int eet_debug_cltrace(int on, long long* out, int* n);
+/* Development trace of the fused decode attention + out-projection
+ * (attn_o.cu): on = 1 resets and enables, on = 0 disables and copies out
+ * up to 4096 records of [sequence, head, start, wait passed, attention done,
+ * contexts gathered, end] (globaltimer ns, one per CTA). */
+int eet_debug_aotrace(int on, long long* out, int* n);
 
 /* ------------------------------------------------------------ layer path */
 typedef struct {

@@ -61,6 +61,7 @@ SIGNATURES = {
     "eet_transpose_cast": (i32, [i32, p, i32, i32, p, p]),
     "eet_debug_launch_chain": (i32, [i32, i32, i32, p, p]),
     "eet_debug_cltrace": (i32, [i32, p, p]),
+    "eet_debug_aotrace": (i32, [i32, p, p]),
     "eet_debug_skip": (i32, [C.c_char_p]),
     "eet_debug_grid_barrier": (i32, [i32, i32, i32, C.POINTER(C.c_float)]),
     "eet_profile_summary": (i32, [i32, C.POINTER(u64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -35,6 +35,17 @@ using namespace sm100;
 
 constexpr int DCH = 64, CW = 8, THREADS = (CW + 1) * 32, XP = 8;
 
+// development trace (eet_debug_aotrace): per CTA globaltimer stamps [start,
+// wait passed, attention done, contexts gathered, end] + (sequence, head)
+__device__ int g_ao_on = 0;
+__device__ unsigned g_ao_n = 0;
+__device__ long long g_ao[4096][8];
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct Args {
   const void* q; int ldq;                  // query row b at q + b * ldq
   const void* kc; const void* vc;          // [b, heads, smax, hd]
@@ -65,6 +76,9 @@ __global__ void __launch_bounds__(THREADS) attn_o_kernel(const __grid_constant__
   const int b0 = b - rank;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / LPK, sub = lane % LPK;
+  const bool trace = g_ao_on && threadIdx.x == 0;
+  long long ts[5] = {0, 0, 0, 0, 0};
+  if (trace) ts[0] = gtime();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NBUF; ++i) {
@@ -120,6 +134,7 @@ __global__ void __launch_bounds__(THREADS) attn_o_kernel(const __grid_constant__
   // ---- consumer warps: online softmax over the key chunks
   griddep_wait();                           // q of this step comes from the QKV GEMV
   griddep_launch_dependents();
+  if (trace) ts[1] = gtime();
   const T* Q = reinterpret_cast<const T*>(a.q) + (long long)b * a.ldq + head * HD;
   const int d0 = sub * E;
   float q[E];
@@ -188,6 +203,7 @@ __global__ void __launch_bounds__(THREADS) attn_o_kernel(const __grid_constant__
     for (int e = 0; e < E; ++e) sm_acc[warp][d0 + e] = acc[e];
   }
   asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");   // consumer warps only
+  if (trace) ts[2] = gtime();
 
   // ---- context row (layer dtype) -> every CTA of the cluster
   if (warp == 0) {
@@ -225,6 +241,7 @@ __global__ void __launch_bounds__(THREADS) attn_o_kernel(const __grid_constant__
   // ---- this head's share of the out-projection: R rows x CB sequences
   mbar_wait(&wbar, 0);
   mbar_wait(&gbar, 0);
+  if (trace) ts[3] = gtime();
   const int g4 = lane >> 2, c4 = lane & 3;
   const bool add_bias = a.bias && head == 0;
   for (int u = warp; u < R / 16; u += CW) {
@@ -242,6 +259,14 @@ __global__ void __launch_bounds__(THREADS) attn_o_kernel(const __grid_constant__
                        : "memory");
         }
       }
+  }
+  if (trace) {
+    ts[4] = gtime();
+    const unsigned i = atomicAdd(&g_ao_n, 1u) & 4095u;
+    g_ao[i][0] = b;
+    g_ao[i][1] = head;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) g_ao[i][2 + j] = ts[j];
   }
 }
 
@@ -327,6 +352,29 @@ bool launch_attn_o(const DecodeArgs& d, const void* wo, int h, long long* acc, l
     else by_depth(__half{}, L8{});
   }
   return true;
+}
+
+extern "C" int eet_debug_aotrace(int on, long long* out, int* n) {
+  // on = 1: reset + enable; on = 0: disable and copy out (4096 x 8)
+  try {
+    if (on) {
+      const int one = 1;
+      const unsigned zero = 0;
+      EET_CHECK_CUDA(cudaMemcpyToSymbol(ao::g_ao_on, &one, sizeof(int)));
+      EET_CHECK_CUDA(cudaMemcpyToSymbol(ao::g_ao_n, &zero, sizeof(unsigned)));
+    } else {
+      const int zero = 0;
+      unsigned cnt = 0;
+      EET_CHECK_CUDA(cudaDeviceSynchronize());
+      EET_CHECK_CUDA(cudaMemcpyToSymbol(ao::g_ao_on, &zero, sizeof(int)));
+      EET_CHECK_CUDA(cudaMemcpyFromSymbol(&cnt, ao::g_ao_n, sizeof(unsigned)));
+      EET_CHECK_CUDA(cudaMemcpyFromSymbol(out, ao::g_ao, sizeof(long long) * 4096 * 8));
+      *n = (int)std::min<unsigned>(cnt, 4096u);
+    }
+    return EET_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  }
 }
 
 }  // namespace eet
