@@ -445,44 +445,74 @@ __global__ void __launch_bounds__(HTHREADS) lm_head_kernel(const __grid_constant
     }
     return;
   }
+  // ---- consumers: final LayerNorm of the token rows -> xs. gamma / beta
+  // of this lane's columns are static: loaded before the wait. Each warp
+  // then takes two rows per pass (w, w+4 / w+8, w+12) with both rows' loads
+  // in flight together: two dependent L2 round trips per warp instead of
+  // eight (every CTA reads the same 16 rows at the same moment).
+  const int nv = K / 4;
+  float4 gg[8], bb[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i = j * 32 + lane;
+    gg[j] = i < nv ? __ldg(reinterpret_cast<const float4*>(ln.g) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    bb[j] = i < nv ? __ldg(reinterpret_cast<const float4*>(ln.b) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   griddep_wait();
   if (trace) ts[1] = gtime();
-
-  // ---- consumers: final LayerNorm of the token rows -> xs (warp w: rows w, w+4, ...)
-  {
-    const int nv = K / 4;
-    for (int r = warp; r < 16; r += HCW) {
-      T* dst = xs + r * xst;
-      if (r >= M) {
-        for (int i = lane; i < nv; i += 32) *reinterpret_cast<uint2*>(dst + i * 4) = make_uint2(0, 0);
-        continue;
-      }
-      const float4* xr = reinterpret_cast<const float4*>(ln.x + r * ln.x_sb);
-      float4 v[8];
+#pragma unroll 1
+  for (int r0 = warp; r0 < 16; r0 += 2 * HCW) {
+    float4 v[2][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = (j * 32 + lane < nv) ? xr[j * 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = 0; p < 2; ++p) {
+      const int r = r0 + p * HCW;
+      const float4* xr = reinterpret_cast<const float4*>(ln.x + (r < M ? r : 0) * ln.x_sb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        v[p][j] = (r < M && j * 32 + lane < nv) ? xr[j * 32 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float sm[2], rs[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
       float s = 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
-      s = warp_sum(s);
-      const float mu = s / (float)K;
+      for (int j = 0; j < 8; ++j) s += (v[p][j].x + v[p][j].y) + (v[p][j].z + v[p][j].w);
+      sm[p] = s;
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) sm[p] = warp_sum(sm[p]) / (float)K;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const float mu = sm[p];
       float qq = 0.f;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (j * 32 + lane < nv) {
-          const float a0 = v[j].x - mu, a1 = v[j].y - mu, a2 = v[j].z - mu, a3 = v[j].w - mu;
+          const float a0 = v[p][j].x - mu, a1 = v[p][j].y - mu, a2 = v[p][j].z - mu, a3 = v[p][j].w - mu;
           qq += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
         }
-      qq = warp_sum(qq);
-      const float rs = 1.0f / sqrtf(qq / (float)K + 1e-5f);
+      rs[p] = qq;
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) rs[p] = 1.0f / sqrtf(warp_sum(rs[p]) / (float)K + 1e-5f);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int r = r0 + p * HCW;
+      T* dst = xs + r * xst;
+      const float mu = sm[p];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int i = j * 32 + lane;
         if (i < nv) {
-          const float4 g4 = __ldg(reinterpret_cast<const float4*>(ln.g) + i);
-          const float4 b4 = __ldg(reinterpret_cast<const float4*>(ln.b) + i);
-          T o[4] = {from_f<T>((v[j].x - mu) * rs * g4.x + b4.x), from_f<T>((v[j].y - mu) * rs * g4.y + b4.y),
-                    from_f<T>((v[j].z - mu) * rs * g4.z + b4.z), from_f<T>((v[j].w - mu) * rs * g4.w + b4.w)};
+          T o[4];
+          if (r < M) {
+            o[0] = from_f<T>((v[p][j].x - mu) * rs[p] * gg[j].x + bb[j].x);
+            o[1] = from_f<T>((v[p][j].y - mu) * rs[p] * gg[j].y + bb[j].y);
+            o[2] = from_f<T>((v[p][j].z - mu) * rs[p] * gg[j].z + bb[j].z);
+            o[3] = from_f<T>((v[p][j].w - mu) * rs[p] * gg[j].w + bb[j].w);
+          } else {
+            o[0] = o[1] = o[2] = o[3] = from_f<T>(0.f);
+          }
           *reinterpret_cast<uint2*>(dst + i * 4) = *reinterpret_cast<const uint2*>(o);
         }
       }
