@@ -355,7 +355,16 @@ def ablation_roofline(step, args, ms_full, w, hbm, torch, _lib):
     h, L, V, es, b = w["hidden"], w["layers"], w["vocab"], 2, w["batch"]
     steps, p = w["steps"], w["prompt"]
     kv = sum(b * 2 * h * es * L * (p + s + 1) for s in range(steps))
-    if os.environ.get("EET_ATTN_O", "1") != "0":
+    if os.environ.get("EET_QKV_ATTN_O", "1") != "0" and h in (512, 1024) and b % 8 == 0:
+        classes = {
+            # decode FFN projections (gemv_cl): W1 (+LN2, GELU), W2 (+residual)
+            "gemv_cl": ("w1,w2", steps * L * 8 * h * h * es, steps * L * 2),
+            # LN1 + QKV + attention + out-projection in one kernel (qkv_attn_o.cu):
+            # every cached K/V row of the batch + W_qkv + W_o once per step
+            "qkv_attn_o": ("qkv,attn,o", kv + steps * L * 4 * h * h * es, steps * L),
+            "lm_head": ("head", steps * V * h * es, steps),
+        }
+    elif os.environ.get("EET_ATTN_O", "1") != "0":
         classes = {
             # decode projections (gemv_cl): QKV (+LN1), W1 (+LN2, GELU), W2 (+residual)
             "gemv_cl": ("qkv,w1,w2", steps * L * 11 * h * h * es, steps * L * 3),

@@ -172,10 +172,13 @@ int eet_debug_launch_chain(int n, int ctas, int pdl, int* counter, void* stream)
  * wait passed, X staged, weights landed, partials sent, end (globaltimer),
  * then clock64 offsets of the phase ends of CTA 0]. */
 int eet_debug_cltrace(int on, long long* out, int* n);
-/* Development trace of the fused decode attention + out-projection
- * (attn_o.cu): on = 1 resets and enables, on = 0 disables and copies out
- * up to 4096 records of [sequence, head, start, wait passed, attention done,
- * contexts gathered, end] (globaltimer ns, one per CTA). */
+/* Development trace of the fused decode kernels: on = 1 resets and
+ * enables, on = 0 disables and copies out (out: 8192 x 8 int64, n: 2 ints)
+ * up to 4096 attn_o.cu records [sequence, head, start, wait passed,
+ * attention done, contexts gathered, end] and, from row 4096, up to 4096
+ * qkv_attn_o.cu records [sequence << 16 | head, start, wait passed, LN
+ * staged, q/k/v reduced, attention done, contexts gathered, end]
+ * (globaltimer ns, one per CTA). */
 int eet_debug_aotrace(int on, long long* out, int* n);
 
 /* ------------------------------------------------------------ layer path */

@@ -25,7 +25,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
-SOURCES = ["rowops.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_tf32.cu", "gemv_tc.cu", "gemv_cl.cu", "attention.cu", "attn_o.cu", "attn_tc.cu", "decode_step.cu", "runtime.cu"]
+SOURCES = ["rowops.cu", "gemm_simt.cu", "gemm_tc.cu", "gemm_tf32.cu", "gemv_tc.cu", "gemv_cl.cu", "attention.cu", "attn_o.cu", "qkv_attn_o.cu", "attn_tc.cu", "decode_step.cu", "runtime.cu"]
 HEADERS = ["eet_internal.h", "common.cuh", "sm100.cuh", "gridsync.cuh", "mma_frag.cuh"]
 
 

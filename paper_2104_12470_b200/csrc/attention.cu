@@ -572,8 +572,10 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32) attn_decode_bulk_kernel(Dec
     if (lane == 0 && a.splits > 1) { part[hd] = M; part[hd + 1] = Lsum; }
   }
   if (a.splits == 1) return;
-  // last split of the pair merges: barrier + one acq_rel atomic (release of
-  // this CTA's partial, acquire of everyone else's) instead of SC fences
+  // last split of the pair merges: the partial's writers (warp 0) fence it
+  // to device scope, then a barrier and one acq_rel atomic (acquire of
+  // everyone else's partials)
+  if (warp == 0) __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     int prev;

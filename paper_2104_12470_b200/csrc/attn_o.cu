@@ -56,6 +56,7 @@ struct Args {
   long long* acc; long long acc_sb;        // pending residual row b at acc + b * acc_sb (2^-32 fixed point)
   const float* bias;                       // b_o (added by head 0) or null
   int R, CB;                               // out rows per CTA, sequences per cluster
+  int pf;                                  // L2 prefetch distance in ring depths (0: off)
 };
 
 template <typename T, int LPK, int NB, int NBUF>
@@ -124,6 +125,14 @@ __global__ void __launch_bounds__(THREADS) attn_o_kernel(const __grid_constant__
         mbar_expect_tx(&full[buf], 2 * bytes);
         bulk_load(dst, Kc + (size_t)c * CH, bytes, &full[buf]);
         bulk_load(dst + CH, Vc + (size_t)c * CH, bytes, &full[buf]);
+        // rolling L2 prefetch a ring's depth ahead: twice the bytes in
+        // flight per (sequence, head) without more shared memory
+        const int cp = c + a.pf * NBUF;
+        if (a.pf && cp < nch) {
+          const uint32_t pb = (uint32_t)(min(DCH, nk - cp * DCH) * HD * sizeof(T));
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Kc + (size_t)cp * CH), "r"(pb) : "memory");
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Vc + (size_t)cp * CH), "r"(pb) : "memory");
+        }
       }
     }
     __syncwarp();
@@ -311,6 +320,11 @@ bool launch_attn_o(const DecodeArgs& d, const void* wo, int h, long long* acc, l
   a.acc = acc; a.acc_sb = acc_sb;
   a.bias = bias;
   a.R = R; a.CB = CB;
+  static const int pf = [] {                       // A/B: EET_AO_PF = L2 prefetch distance (ring depths)
+    const char* v = std::getenv("EET_AO_PF");
+    return v ? std::max(0, std::min(4, atoi(v))) : 0;
+  }();
+  a.pf = pf;
   const CUtensorMap mw = make_tma_map_2d(wo, h, hq, hq, R, d.dtype);
   double keys = 0;
   if (d.L_host >= 0)
@@ -354,9 +368,13 @@ bool launch_attn_o(const DecodeArgs& d, const void* wo, int h, long long* acc, l
   return true;
 }
 
+void qao_trace(int on, long long* out, int* n);
+
 extern "C" int eet_debug_aotrace(int on, long long* out, int* n) {
-  // on = 1: reset + enable; on = 0: disable and copy out (4096 x 8)
+  // on = 1: reset + enable; on = 0: disable and copy out: attn_o records
+  // [0, 4096) x 8, qkv_attn_o records [4096, 8192) x 8; n[0], n[1] counts
   try {
+    qao_trace(on, on ? nullptr : out + 4096 * 8, on ? nullptr : n + 1);
     if (on) {
       const int one = 1;
       const unsigned zero = 0;

@@ -223,6 +223,13 @@ bool launch_attn_o(const DecodeArgs& a, const void* wo, int h, long long* acc, l
 bool gemv_cl(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
              long long x_sb, long long x_ss, const int2* rinfo, const float* g, const float* b, const Epi& e,
              cudaStream_t st, const long long* acc = nullptr, long long acc_sb = 0);
+// decode LN1 + QKV + attention + out-projection in one kernel (qkv_attn_o.cu)
+bool qkv_attn_o_ok(int dtype, int batch, int h, int heads, int hd, int hq, const float* x, long long x_sb,
+                   const void* kc, const void* vc, const void* wqkv, const void* wo);
+bool launch_qkv_attn_o(int dtype, int batch, int h, int heads, int smax, const float* x, long long x_sb,
+                       const float* g, const float* bl, const void* wqkv, const float* bqkv, void* kc, void* vc,
+                       const int* pads, const int* kv_start, int kv_base, const void* wo, const float* bo,
+                       long long* acc, long long acc_sb, int L_host, const int* h_pads, cudaStream_t st);
 // would gemv_cl take this projection (same checks, no launch)
 bool gemv_cl_ok(int dtype, const void* W, int M, int N, int K, const void* X, int ldx, const float* x,
                 long long x_sb, const float* g, const float* b, int mode);

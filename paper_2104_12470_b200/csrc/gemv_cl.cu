@@ -531,6 +531,14 @@ __global__ void __launch_bounds__(HTHREADS) lm_head_kernel(const __grid_constant
   for (int i = warp; i < nmine; i += HCW) {
     const int st = i % HSTAGES;
     const int t = blockIdx.x + i * gridDim.x;
+    // A stage's successive tiles go to different consumer warps (HSTAGES is
+    // not a multiple of HCW), so this warp can be two phases ahead of the
+    // stage: tile i - HSTAGES (another warp's) may not even have landed yet,
+    // and a parity wait on `full` alone would then pass on the older phase
+    // and read the wrong tile. Waiting first for that tile's release
+    // (the producer's own condition) makes the full-barrier parity
+    // unambiguous.
+    if (i >= HSTAGES) mbar_wait(&empty[st], (uint32_t)(((i / HSTAGES) - 1) & 1));
     mbar_wait(&full[st], (uint32_t)((i / HSTAGES) & 1));
     float acc[NB][4];
     warp_mma<T, NB>(smem_u32(smem + st * stage_bytes), 16, 0, 0, K / 16, xs, xst, lane, acc);

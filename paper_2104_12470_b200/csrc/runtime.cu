@@ -613,7 +613,30 @@ static bool attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
   const int scope = (p.phase == EET_PHASE_PROMPT) ? EET_SCOPE_WITHIN : EET_SCOPE_ACROSS;
   if (T == 0) return false;
 
+  // decode: the whole attention half in one kernel (qkv_attn_o.cu), or the
+  // attention + out-projection in one (attn_o.cu), when the FFN GEMVs that
+  // consume the pending out-projection take this shape
+  const bool inc = p.phase == EET_PHASE_INCREMENTAL;
+  const bool pend_ok = inc && !keep_ctx && !partial && (x_ss & 3) == 0 && !skip_decode("o") &&
+                       gemv_cl_ok(dt, w->w1, T, rt->ffn, h, nullptr, 0, x, x_sb, w->ln2_g, w->ln2_b, EPI_GELU_T) &&
+                       gemv_cl_ok(dt, w->w2, T, h, rt->ffn, nullptr, rt->ffn, nullptr, 0, nullptr, nullptr, EPI_RESID);
+  const bool fuse_all = pend_ok && rt->splits == 1 && T == p.batch && !skip_decode("qkv") && !skip_decode("attn") &&
+                        qkv_attn_o_ok(dt, T, h, rt->heads, rt->hd, hq, x, x_sb, kc, vc, w->wqkv, w->wo);
+  if (pend_ok && !rt->oacc) {
+    rt->oacc = (long long*)rt->dev(sizeof(long long) * (size_t)rt->bmax * h);
+    EET_CHECK_CUDA(cudaMemsetAsync(rt->oacc, 0, sizeof(long long) * (size_t)rt->bmax * h, st));
+  }
   Claim q(rt->pool, (size_t)T * hq * es, scope, "attention.query");
+  if (fuse_all) {
+    Claim ctx(rt->pool, (size_t)T * hq * es, scope, "attention.context");
+    const bool ok = launch_qkv_attn_o(dt, T, h, rt->heads, rt->smax, x, x_sb, w->ln1_g, w->ln1_b, w->wqkv, w->b_qkv,
+                                      kc, vc, p.pads, kv_dev, kv_base, w->wo, w->b_o, rt->oacc, h, L_host,
+                                      p.h_pads.data(), st);
+    EET_REQUIRE(ok, EET_ERR_UNSUPPORTED, "fused decode attention rejected an eligible shape");
+    ctx.release();
+    q.release();
+    return true;
+  }
   {
     Epi e;
     e.mode = EPI_QKV;
@@ -629,7 +652,6 @@ static bool attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     e.kv_start = kv_dev;
     e.kv_base = kv_base;
     // decode rows: LN1 runs inside the GEMV prologue; otherwise LN -> GEMM
-    const bool inc = p.phase == EET_PHASE_INCREMENTAL;
     if (inc && skip_decode("qkv")) {
     } else if (inc && gemv_cl(dt, w->wqkv, T, 3 * hq, h, nullptr, 0, x, x_sb, x_ss, p.rinfo, w->ln1_g, w->ln1_b,
                               e, st)) {
@@ -684,21 +706,10 @@ static bool attn_block(eet_runtime* rt, const StepPlan& p, float* x, long long x
     a.o = ctx.ptr; a.ldo = hq;
     a.splits = rt->splits;
     if (!skip_decode("attn")) {
-      // out-projection fused into the attention kernel (attn_o.cu) when the
-      // FFN GEMVs that consume its pending result take this shape
-      const int f = rt->ffn;
-      if (!keep_ctx && !partial && !skip_decode("o") && (x_ss & 3) == 0 &&
-          gemv_cl_ok(dt, w->w1, T, f, h, nullptr, 0, x, x_sb, w->ln2_g, w->ln2_b, EPI_GELU_T) &&
-          gemv_cl_ok(dt, w->w2, T, h, f, nullptr, f, nullptr, 0, nullptr, nullptr, EPI_RESID)) {
-        if (!rt->oacc) {
-          rt->oacc = (long long*)rt->dev(sizeof(long long) * (size_t)rt->bmax * h);
-          EET_CHECK_CUDA(cudaMemsetAsync(rt->oacc, 0, sizeof(long long) * (size_t)rt->bmax * h, st));
-        }
-        if (launch_attn_o(a, w->wo, h, rt->oacc, h, w->b_o, st)) {
-          q.release();
-          ctx.release();
-          return true;
-        }
+      if (pend_ok && launch_attn_o(a, w->wo, h, rt->oacc, h, w->b_o, st)) {
+        q.release();
+        ctx.release();
+        return true;
       }
       launch_attn_decode(a, st);
     }

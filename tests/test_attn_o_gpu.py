@@ -1,13 +1,13 @@
-"""Decode attention fused with the out-projection (csrc/attn_o.cu) through the
-layer API: prompt pass + incremental steps against the fp32 oracle, and
-bit-identical repeats (the heads' out-projection contributions are summed as
-2^-32 fixed-point integer atomics, so their arrival order cannot change the
-result).
+"""Fused decode kernels through the layer API: prompt pass + incremental
+steps against the fp32 oracle, and bit-identical repeats (the heads'
+out-projection contributions are summed as 2^-32 fixed-point integer
+atomics, so their arrival order cannot change the result).
 
-Shapes where the fused kernel is taken (16-bit, head_dim 64, one CTA per
-(sequence, head) fills the GPU, <= 16 decode rows): GPT-2-medium width at
-b16 (clusters of 8 sequences, 128 W_o rows per CTA) and h2048 / 32 heads at
-b8 (256 W_o rows per CTA, two row tiles per warp).
+* GPT-2-medium width at b16 (fp16, bf16): LayerNorm 1 + QKV + attention +
+  out-projection in one kernel (csrc/qkv_attn_o.cu; hidden 512/1024,
+  clusters of 8 sequences, split-K QKV over the cluster);
+* h2048 / 32 heads at b8 (bf16): attention + out-projection (csrc/attn_o.cu,
+  256 W_o rows per CTA, two row tiles per warp) after the QKV GEMV.
 
 Reference: /root/reference/pkg/src/maskfold/runtime.py:160-188 (attention,
 context @ W_o into the residual), :217-263 (the layer).

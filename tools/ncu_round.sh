@@ -19,7 +19,7 @@ done
 # full captures of the top kernels (skip the warm-up call's launches)
 timeout 600 $NCU $FULL -k regex:gemv_cl -s 400 -c 4 -o $O/gemv_cl_c2 -f python tools/decode_profile.py --steps 4 > $O/gemv_cl_c2.log 2>&1
 timeout 600 $NCU $FULL -k regex:lm_head -s 3 -c 1 -o $O/lm_head_c2 -f python tools/decode_profile.py --steps 4 > $O/lm_head_c2.log 2>&1
-timeout 600 $NCU $FULL -k regex:attn_o -s 60 -c 2 -o $O/attn_o_c2 -f python tools/decode_profile.py --steps 4 > $O/attn_o_c2.log 2>&1
+timeout 600 $NCU $FULL -k regex:qkv_attn_o -s 60 -c 2 -o $O/qkv_attn_o_c2 -f python tools/decode_profile.py --steps 4 > $O/qkv_attn_o_c2.log 2>&1
 timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c3 -f python tools/layer_profile.py --workload c3 > $O/attn_tc_c3.log 2>&1
 timeout 600 $NCU $FULL -k regex:gemm_tc -s 4 -c 4 -o $O/gemm_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/gemm_tc_c4.log 2>&1
 timeout 600 $NCU $FULL -k regex:attn_tc -s 1 -c 1 -o $O/attn_tc_c4 -f python tools/layer_profile.py --workload c4 > $O/attn_tc_c4.log 2>&1

@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_summary  # noqa: E402
 
 KIND = [("gemv_cl", "gemv_cl"), ("lm_head", "lm_head"), ("gemm_tc", "gemm_tc"), ("attn_tc", "attn_prefill"),
-        ("attn_decode", "attn_decode"), ("attn_o", "attn_o"), ("gemv", "gemv"), ("ln_rows", "layernorm"), ("layernorm", "layernorm"),
+        ("attn_decode", "attn_decode"), ("qkv_attn_o", "qkv_attn_o"), ("attn_o", "attn_o"), ("gemv", "gemv"), ("ln_rows", "layernorm"), ("layernorm", "layernorm"),
         ("argmax", "argmax")]
 
 
