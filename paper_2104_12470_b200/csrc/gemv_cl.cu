@@ -310,11 +310,20 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
     } else {
       const T* X = reinterpret_cast<const T*>(sh.X);
       const int cpr = Kc / 8;                                   // 16-byte chunks per row
-      for (int i = threadIdx.x; i < 16 * cpr; i += THREADS) {
-        const int r = i / cpr, c = i - r * cpr;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (r < sh.M && !dry) v = *reinterpret_cast<const uint4*>(X + (size_t)r * sh.ldx + k0 + c * 8);
-        *reinterpret_cast<uint4*>(xs + r * xst + c * 8) = v;
+      // all of this thread's chunks in flight before the first shared store
+      // (Kc <= 512: at most 4 per thread; one L2 round trip, not four)
+      constexpr int XV = 4;
+      uint4 tmp[XV];
+#pragma unroll
+      for (int k = 0; k < XV; ++k) {
+        const int i = threadIdx.x + k * THREADS, r = i / cpr, c = i - r * cpr;
+        tmp[k] = make_uint4(0, 0, 0, 0);
+        if (i < 16 * cpr && r < sh.M && !dry) tmp[k] = *reinterpret_cast<const uint4*>(X + (size_t)r * sh.ldx + k0 + c * 8);
+      }
+#pragma unroll
+      for (int k = 0; k < XV; ++k) {
+        const int i = threadIdx.x + k * THREADS, r = i / cpr, c = i - r * cpr;
+        if (i < 16 * cpr) *reinterpret_cast<uint4*>(xs + r * xst + c * 8) = tmp[k];
       }
     }
     __syncwarp();
@@ -364,10 +373,38 @@ __global__ void __launch_bounds__(THREADS) gemv_cl_kernel(const __grid_constant_
       const int t = q / NB, nb = q - t * NB;
       const int row = t * 16 + (ln_ >> 2), tok = nb * 8 + 2 * (ln_ & 3);
       const float vv[4] = {v.x, v.y, v.z, v.w};
+      if constexpr (MODE == EPI_RESID) {
+        // residual read-modify-write: the four elements' loads (x, and the
+        // pending out-projection) all in flight before any store — one L2
+        // round trip instead of four (the elements are distinct)
+        float xv[4];
+        long long av[4];
+        bool ok[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int n = r0 + row + 8 * (i >> 1), m = tok + (i & 1);
+          ok[i] = n < sh.N && m < sh.M && !dry;
+          xv[i] = ok[i] ? e.x[m * e.x_sb + n] : 0.f;
+          av[i] = (ok[i] && e.acc) ? e.acc[m * e.acc_sb + n] : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (!ok[i]) continue;
+          const int n = r0 + row + 8 * (i >> 1), m = tok + (i & 1);
+          const float val = e.bias ? vv[i] + e.bias[n] : vv[i];
+          if (e.acc) {
+            e.x[m * e.x_sb + n] = (xv[i] + acc_to_f(av[i])) + val;
+            e.acc[m * e.acc_sb + n] = 0;
+          } else {
+            e.x[m * e.x_sb + n] = xv[i] + val;
+          }
+        }
+      } else {
 #pragma unroll 1
-      for (int i = 0; i < 4; ++i) {                    // rolled: one copy of the epilogue code
-        const int n = r0 + row + 8 * (i >> 1), m = tok + (i & 1);
-        if (n < sh.N && m < sh.M && !dry) dec_epi<T, MODE>(e, kvs, m, n, vv[i]);
+        for (int i = 0; i < 4; ++i) {                  // rolled: one copy of the epilogue code
+          const int n = r0 + row + 8 * (i >> 1), m = tok + (i & 1);
+          if (n < sh.N && m < sh.M && !dry) dec_epi<T, MODE>(e, kvs, m, n, vv[i]);
+        }
       }
     }
   }
