@@ -118,6 +118,49 @@ __device__ __forceinline__ uint64_t cvt2(uint32_t w) {
   }
 }
 
+// q.k over two packed 16-bit pairs with fp32 accumulation and no conversion
+// (FHFMA: the f16/bf16 products are exact in fp32, as after a conversion)
+template <typename T>
+__device__ __forceinline__ void hdot2(uint32_t q, uint32_t k, float& d0, float& d1) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    asm("{\n .reg .b16 ql, qh, kl, kh;\n mov.b32 {ql, qh}, %2;\n mov.b32 {kl, kh}, %3;\n"
+        " fma.rn.f32.bf16 %0, ql, kl, %0;\n fma.rn.f32.bf16 %1, qh, kh, %1;\n}"
+        : "+f"(d0), "+f"(d1) : "r"(q), "r"(k));
+  } else {
+    asm("{\n .reg .b16 ql, qh, kl, kh;\n mov.b32 {ql, qh}, %2;\n mov.b32 {kl, kh}, %3;\n"
+        " fma.rn.f32.f16 %0, ql, kl, %0;\n fma.rn.f32.f16 %1, qh, kh, %1;\n}"
+        : "+f"(d0), "+f"(d1) : "r"(q), "r"(k));
+  }
+}
+template <typename T>
+__device__ __forceinline__ uint32_t pack16(float a, float b) {
+  T v[2] = {from_f<T>(a), from_f<T>(b)};
+  return *reinterpret_cast<const uint32_t*>(v);
+}
+// four chains over E = 16 dims (8 packed words). fp16 uses the mixed FMA;
+// bf16 converts (the bf16 form measured worse against the fp32 oracle at
+// GPT-2-medium depth: elementwise ratio 2.2 vs 1.7 for the format itself)
+template <typename T>
+__device__ __forceinline__ float hdot16(const uint32_t* q, const uint32_t* k) {
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    uint64_t d2 = f2pack(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d2 = ffma2(cvt2<T>(q[i]), cvt2<T>(k[i]), d2);
+    float lo, hi;
+    f2unpack(d2, lo, hi);
+    return lo + hi;
+  } else {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      hdot2<T>(q[i], k[i], a0, a1);
+      hdot2<T>(q[i + 1], k[i + 1], a2, a3);
+    }
+    return (a0 + a1) + (a2 + a3);
+  }
+}
+
+
 __device__ __forceinline__ void st_async_b32(uint32_t addr, float v, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr),
                "r"(__float_as_uint(v)), "r"(mbar)
@@ -322,14 +365,16 @@ __global__ void __launch_bounds__(THREADS) qkv_attn_o_kernel(const __grid_consta
   if (trace) ts[3] = gtime();
 
   // 4. online softmax: earlier keys from the ring, then this step's key.
-  //    Packed f32x2 arithmetic (FFMA2) for q.k and p.v, and the running
+  //    q.k as mixed-precision FMAs on the 16-bit operands (no conversions),
+  //    packed f32x2 arithmetic (FFMA2) for p.v, and the running
   //    maximum rescales the accumulators only when it grows (corr would be
   //    exactly 1 otherwise): the chain per key is ~2/3 of the scalar form.
   const int g = lane / LPK, sub = lane % LPK, d0 = sub * E;
-  uint64_t q2[E / 2], acc2[E / 2];
+  uint32_t qh[E / 2];                      // q in the layer dtype (it was rounded to it)
+  uint64_t acc2[E / 2];
 #pragma unroll
   for (int i = 0; i < E / 2; ++i) {
-    q2[i] = f2pack(qkvf[d0 + 2 * i], qkvf[d0 + 2 * i + 1]);
+    qh[i] = pack16<T>(qkvf[d0 + 2 * i], qkvf[d0 + 2 * i + 1]);
     acc2[i] = f2pack(0.f, 0.f);
   }
   float m = -INFINITY, l = 0.f;
@@ -366,12 +411,7 @@ __global__ void __launch_bounds__(THREADS) qkv_attn_o_kernel(const __grid_consta
       }
       const uint32_t* kw = reinterpret_cast<const uint32_t*>(kr);
       const uint32_t* vw = reinterpret_cast<const uint32_t*>(vr);
-      uint64_t d2 = f2pack(0.f, 0.f);
-#pragma unroll
-      for (int i = 0; i < E / 2; ++i) d2 = ffma2(q2[i], cvt2<T>(kw[i]), d2);
-      float dlo, dhi;
-      f2unpack(d2, dlo, dhi);
-      float dot = dlo + dhi;
+      float dot = hdot16<T>(qh, kw);
 #pragma unroll
       for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
       if (ok) {
@@ -385,13 +425,10 @@ __global__ void __launch_bounds__(THREADS) qkv_attn_o_kernel(const __grid_consta
     if (lane == 0) mbar_arrive(&empty[buf]);
   }
   if (warp == 0) {                          // this step's key: group 0 of warp 0
-    uint64_t d2 = f2pack(0.f, 0.f);
+    uint32_t kh[E / 2];
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i)
-      d2 = ffma2(q2[i], f2pack(qkvf[HD + d0 + 2 * i], qkvf[HD + d0 + 2 * i + 1]), d2);
-    float dlo, dhi;
-    f2unpack(d2, dlo, dhi);
-    float dot = dlo + dhi;
+    for (int i = 0; i < E / 2; ++i) kh[i] = pack16<T>(qkvf[HD + d0 + 2 * i], qkvf[HD + d0 + 2 * i + 1]);
+    float dot = hdot16<T>(qh, kh);
 #pragma unroll
     for (int o = 1; o < LPK; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (g == 0) {
