@@ -294,8 +294,12 @@ typedef struct {
 } eet_model;
 
 /* generate (runtime.py:372-437): one prompt pass, then `steps` incremental
- * steps captured once into a CUDA graph and replayed. Greedy argmax with
- * the lowest id on ties. h_prompts: HOST int32 [batch, max_len] padded with
+ * steps captured once into a CUDA graph and replayed. In 16-bit modes a
+ * decode step is embed -> per layer [LN1 + QKV + attention + out-projection
+ * in one kernel, LN2 + W1, W2] -> LN + LM head + argmax (where the shapes
+ * allow; the five-launch layer otherwise). Deterministic: repeated calls
+ * give bit-identical tokens and logits. Greedy argmax with the lowest id on
+ * ties. h_prompts: HOST int32 [batch, max_len] padded with
  * anything past each length; h_lengths: HOST int32[batch].
  * h_tokens: HOST int64 [batch, steps] (written on return).
  * d_logits: optional DEVICE fp32 [steps, batch, vocab] (may be NULL).
