@@ -57,16 +57,18 @@ def _run(eet, w, cfg, desc, x, steps_x):
     return outs
 
 
-@pytest.mark.parametrize("h,heads,b,dt", [(1024, 16, 16, "fp16"), (1024, 16, 16, "bf16"),
-                                          (2048, 32, 8, "bf16")])
-def test_fused_decode_steps_vs_oracle(eet, h, heads, b, dt):
+@pytest.mark.parametrize("h,heads,b,bmax,dt", [(1024, 16, 16, 16, "fp16"), (1024, 16, 16, 16, "bf16"),
+                                               (1024, 16, 8, 16, "fp16"), (2048, 32, 8, 8, "bf16")])
+def test_fused_decode_steps_vs_oracle(eet, h, heads, b, bmax, dt):
+    """bmax: the configuration's batch (capacity); b < bmax runs one cluster
+    of 8 sequences per head on a runtime sized for 16."""
     from oracle import eet_oracle as orc
     s, nsteps = 96, 3
     rng = np.random.default_rng(h + b)
     lengths = [s] + [int(n) for n in rng.integers(1, s + 1, size=b - 1)]
     desc = eet.make_batch(lengths)
     w = _layer(eet, h, 7)
-    cfg = eet.ModelConfig(batch_size=b, hidden_size=h, layer_count=1, head_count=heads, max_prompt=s,
+    cfg = eet.ModelConfig(batch_size=bmax, hidden_size=h, layer_count=1, head_count=heads, max_prompt=s,
                           max_sequence=s + nsteps, datatype_label=dt)
     x = rng.standard_normal(size=(b, s, h), dtype=np.float32)
     steps_x = [rng.standard_normal(size=(b, 1, h), dtype=np.float32) for _ in range(nsteps)]
